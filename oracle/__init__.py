@@ -1,0 +1,173 @@
+"""ctypes loader for the CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+leg may import this module.  The product path (paper_2507_21276_b200) never
+imports, links or executes anything under oracle/.
+
+The oracle itself is plain C (oracle/lemix_oracle.c), written from PAPER.md
+Algorithm 1 and Eq. 1-4; see its header for the citations.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "liblemix_oracle.so")
+_lib = None
+
+LEMIX, RR, SEPARATE, FIXED = 0, 1, 2, 3
+OK, EINVAL, EQCAP, EBUDGET = 0, 1, 6, 7
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("n_nodes", ctypes.c_int32), ("n_stages", ctypes.c_int32),
+                ("eta_f", ctypes.c_void_p), ("eta_b", ctypes.c_void_p)]
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("policy", ctypes.c_int32), ("deprioritize", ctypes.c_int32),
+                ("slo_mode", ctypes.c_int32), ("qcap", ctypes.c_int32),
+                ("lambda1", ctypes.c_double), ("lambda2", ctypes.c_double), ("tau", ctypes.c_double),
+                ("slo_mult", ctypes.c_double), ("slo_const", ctypes.c_double),
+                ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double)]
+
+
+SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes",
+               "sum_version", "status")
+SUMMARY_F64 = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util",
+               "mean_len_std")
+
+
+class Summary(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in SUMMARY_INT] + [(k, ctypes.c_double) for k in SUMMARY_F64]
+
+
+COUNTERS = ("decisions", "alg1_calls", "stage_iters", "scan_consumed", "scan_break", "offset_adds",
+            "lc_exp", "lc_cold", "commits_train", "eq4_checks", "deferrals", "version_scan", "max_qlen")
+
+
+class Counters(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int64) for k in COUNTERS]
+
+
+SUMMARY_DTYPE = np.dtype([(k, np.int64) for k in SUMMARY_INT] + [(k, np.float64) for k in SUMMARY_F64])
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError(f"{_LIB_PATH} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(_LIB_PATH)
+        vp = ctypes.c_void_p
+        lib.orc_run_trace.restype = ctypes.c_int
+        lib.orc_run_trace.argtypes = [ctypes.POINTER(Profile), ctypes.POINTER(Params), ctypes.c_int64,
+                                      ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      ctypes.POINTER(Summary), ctypes.POINTER(Counters)]
+        lib.orc_run_batch.restype = ctypes.c_int
+        lib.orc_run_batch.argtypes = [ctypes.POINTER(Profile), ctypes.POINTER(Params), ctypes.c_int64,
+                                      vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(Counters)]
+        lib.orc_exp_neg.restype = ctypes.c_double
+        lib.orc_exp_neg.argtypes = [ctypes.c_double]
+        _lib = lib
+    return _lib
+
+
+@dataclass
+class OracleParams:
+    policy: int = LEMIX
+    lambda1: float = 1.0
+    lambda2: float = 1.0
+    tau: float = 0.0
+    slo_mult: float = 5.0
+    sigma_floor: float = 1.0
+    lc0: float = 0.0
+    alpha: float = 0.5
+    deprioritize: int = 1
+    slo_mode: int = 0
+    qcap: int = 512
+    slo_const: float = 0.0
+
+    def _c(self) -> Params:
+        return Params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1,
+                      self.lambda2, self.tau, self.slo_mult, self.slo_const, self.sigma_floor,
+                      self.lc0, self.alpha)
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def exp_neg(t: float) -> float:
+    return _load().orc_exp_neg(float(t))
+
+
+def run_trace(eta_f, eta_b, n_nodes, n_stages, arrival, lbk, n_inf, params: OracleParams,
+              fixed_node=None, want_paths=False, want_cand=False):
+    """Run one trace; returns a dict of per-task outputs, summary, counters."""
+    lib = _load()
+    eta_f = np.ascontiguousarray(eta_f, np.float64)
+    eta_b = np.ascontiguousarray(eta_b, np.float64)
+    arrival = np.ascontiguousarray(arrival, np.float64)
+    lbk = np.ascontiguousarray(lbk, np.uint32)
+    m = len(arrival)
+    prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data)
+    par = params._c()
+    node_defer = np.zeros(m, np.uint32)
+    dec = np.full(m, -1, np.int32)
+    comp = np.zeros(m, np.float64)
+    sf1 = np.zeros(m, np.float64)
+    paths = np.zeros(m * n_stages * 4, np.float64) if want_paths else None
+    cand = np.zeros(max(m, 1) * n_nodes * 3, np.float64) if want_cand else None
+    fixed = None if fixed_node is None else np.ascontiguousarray(fixed_node, np.int32)
+    sm = Summary()
+    ct = Counters()
+    st = lib.orc_run_trace(ctypes.byref(prof), ctypes.byref(par), m, int(n_inf), arrival.ctypes.data,
+                           lbk.ctypes.data, _ptr(fixed), node_defer.ctypes.data, dec.ctypes.data,
+                           comp.ctypes.data, sf1.ctypes.data, _ptr(paths), _ptr(cand), ctypes.byref(sm),
+                           ctypes.byref(ct))
+    out = dict(status=st, node=(node_defer & 0xFFFF).astype(np.int32), defer=(node_defer >> 16).astype(np.int32),
+               node_defer=node_defer, decision_idx=dec, completion=comp, start_f1=sf1,
+               summary={k: getattr(sm, k) for k in SUMMARY_INT + SUMMARY_F64},
+               counters={k: getattr(ct, k) for k in COUNTERS})
+    if want_paths:
+        out["paths"] = paths.reshape(m, n_stages, 4)
+    if want_cand:
+        out["cand"] = cand.reshape(max(m, 1), n_nodes, 3)[:m]
+    return out
+
+
+def run_batch(eta_f, eta_b, n_nodes, n_stages, traces, params: OracleParams, fixed_node=None,
+              outputs=True):
+    """Run a CSR batch (workload.Traces).  Returns (summaries structured array,
+    per-task dict or None, counters dict, first error status)."""
+    lib = _load()
+    eta_f = np.ascontiguousarray(eta_f, np.float64)
+    eta_b = np.ascontiguousarray(eta_b, np.float64)
+    prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data)
+    par = params._c()
+    m = traces.n_tasks
+    T = traces.n_traces
+    sums = np.zeros(T, SUMMARY_DTYPE)
+    ct = Counters()
+    node_defer = np.zeros(m, np.uint32) if outputs else None
+    dec = np.full(m, -1, np.int32) if outputs else None
+    comp = np.zeros(m, np.float64) if outputs else None
+    sf1 = np.zeros(m, np.float64) if outputs else None
+    fixed = None if fixed_node is None else np.ascontiguousarray(fixed_node, np.int32)
+    offsets = np.ascontiguousarray(traces.offsets, np.int64)
+    n_inf = np.ascontiguousarray(traces.n_inf, np.int32)
+    arrival = np.ascontiguousarray(traces.arrival, np.float64)
+    lbk = np.ascontiguousarray(traces.lbk, np.uint32)
+    st = lib.orc_run_batch(ctypes.byref(prof), ctypes.byref(par), T, offsets.ctypes.data,
+                           n_inf.ctypes.data, arrival.ctypes.data, lbk.ctypes.data, _ptr(fixed),
+                           _ptr(node_defer), _ptr(dec), _ptr(comp), _ptr(sf1), sums.ctypes.data,
+                           ctypes.byref(ct))
+    per_task = None
+    if outputs:
+        per_task = dict(node_defer=node_defer, decision_idx=dec, completion=comp, start_f1=sf1)
+    return sums, per_task, {k: getattr(ct, k) for k in COUNTERS}, st

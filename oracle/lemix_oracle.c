@@ -1,0 +1,526 @@
+/*
+ * lemix_oracle.c -- TEST INFRASTRUCTURE ONLY (see lemix_oracle.h).
+ *
+ * A plain, slow, obviously-correct, single-threaded CPU implementation of the
+ * LeMix placement step, written from the paper (arXiv 2507.21276, file
+ * /root/reference/PAPER.md) in the paper's order and notation:
+ *
+ *   - latency model            Δ_F = η_F^n·C·ℓ², Δ_B = η_B^n·C·ℓ²     PAPER.md:383 (§4.1)
+ *   - ComputeIdleness          Algorithm 1, lines 1-21                PAPER.md:432-476 (§4.2)
+ *   - backward planning                                                PAPER.md:490-491 (§4.2)
+ *   - idleness profit IP       Eq. 1 (eq:idle_profit)                 PAPER.md:544-549 (§4.3)
+ *   - length consistency LC    Eq. 2 (eq:length_heterogeneity)        PAPER.md:552-557 (§4.3)
+ *   - node priority f          Eq. 3 (eq:node_fitness), highest wins  PAPER.md:562-568 (§4.3)
+ *   - queue-level deprioritise Eq. 4                                   PAPER.md:586-597 (§4.3)
+ *   - global queue order       inference by arrival, training by the
+ *                              previous training task's S1 forward end PAPER.md:224 (§3)
+ *   - baselines Separate / NaiveMix(RR)                                PAPER.md:795-796 (§6.1)
+ *   - metrics (throughput, SLO = TTFT <= 5x forward latency)          PAPER.md:786-790 (§6.1)
+ *
+ * Where the paper is silent or garbled the DESIGN.md reading is cited as
+ * [R-n] (DESIGN.md §"Readings").  Floating point: IEEE binary64, built with
+ * -O2 -ffp-contract=off (no FMA contraction, no reassociation).  The
+ * expression forms follow DESIGN.md §"Canonical fp64 expression sheet".
+ *
+ * Data structures are deliberately literal: per-node trace queues hold task
+ * indices (Q^n, Q_train^n), Q_temp is a fresh copy per call, removal is a
+ * list deletion, every task keeps its full planned path.  Nothing here is
+ * blocked, fused or reordered.
+ */
+#include "lemix_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define MAXS 16
+
+/* MAX/MIN as ternaries ([R-maxmin]: fmax/fmin leave the sign of zero unspecified). */
+static double MAX(double x, double y) { return (y > x) ? y : x; }
+static double MIN(double x, double y) { return (y < x) ? y : x; }
+
+/* ---------------------------------------------------------------------------
+ * exp(-t), t >= 0: the fully specified routine of DESIGN.md [R-exp]
+ * (Cody-Waite reduction by ln 2, degree-13 Taylor polynomial in Horner form,
+ * multiply then add, no FMA; exact scaling by 2^k).  Pinned against libm in
+ * tests/test_oracle_units.py (<= 2 ulp) and exact at t = 0.
+ * ------------------------------------------------------------------------- */
+double orc_exp_neg(double t)
+{
+    static const double C[14] = {
+        0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5,
+        0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+        0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
+        0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};
+    if (t > 700.0) return 0.0;
+    double x = -t;
+    double k = rint(x * 0x1.71547652b82fep0);       /* round half to even */
+    double hi = x - k * 0x1.62e42fee00000p-1;      /* ln2 high part */
+    double lo = k * 0x1.a39ef35793c76p-33;         /* ln2 low part */
+    double r = hi - lo;
+    double p = C[13];
+    for (int i = 12; i >= 0; --i) p = p * r + C[i];
+    return ldexp(p, (int)k);
+}
+
+/* ---------------------------------------------------------------------------
+ * Per-trace state
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    double sf[MAXS], ef[MAXS];   /* forward path  start_f^s, end_f^s */
+    double sb[MAXS], eb[MAXS];   /* backward path start_b^s, end_b^s (training only) */
+} path_t;
+
+typedef struct {
+    int64_t last_task;      /* Q^n[-1], -1 if the node never ran a task */
+    double a_last;          /* a_[-1]: dispatch time of that task (Eq. 1, [R-9]) */
+    int has_efS;            /* Q^n non-empty */
+    double max_efS;         /* max over task in Q^n of end_f^S (Eq. 4 inner max, [R-14]) */
+    int64_t *q_train;       /* Q_train^n: task indices, enqueue order */
+    int64_t q_len;
+    int64_t hist_cnt, hist_sum, hist_sumsq;   /* lengths of tasks previously run here ([R-10]) */
+    double busy[MAXS];
+    int64_t n_train_on;     /* training tasks committed here (co-located model version) */
+} node_t;
+
+typedef struct {
+    const orc_profile *prof;
+    const orc_params *par;
+    int N, S;
+    const double *arrival;
+    const uint32_t *lbk;
+    path_t *path;           /* per task */
+    node_t *node;
+    orc_counters *cnt;
+} trace_t;
+
+static int task_len(uint32_t v) { return (int)(v & 0xFFFu); }
+static int task_batch(uint32_t v) { return (int)((v >> 12) & 0xFFu); }
+static int task_kind(uint32_t v) { return (int)((v >> 20) & 1u); }
+
+/* C·ℓ² as an exact double (< 2^53). */
+static double task_w(uint32_t v)
+{
+    int64_t l = task_len(v), C = task_batch(v);
+    return (double)(C * l * l);
+}
+
+static double eta_f(const trace_t *T, int n, int s) { return T->prof->eta_f[n * T->S + s]; }
+static double eta_b(const trace_t *T, int n, int s) { return T->prof->eta_b[n * T->S + s]; }
+
+/* ---------------------------------------------------------------------------
+ * Algorithm 1  ComputeIdleness.  Line numbers below are
+ * the algorithm's own.  Returns II and R; writes the planned forward path of
+ * the new task into sf/ef.  Entries of Q_train^n for which CheckExecuted holds
+ * (lines 17-18) are removed from the node's queue on return.
+ * ------------------------------------------------------------------------- */
+static void compute_idleness(trace_t *T, int n, uint32_t task_lbk, double a, double now,
+                             double *II_out, double *R_out, double *sf, double *ef)
+{
+    const int S = T->S;
+    node_t *nd = &T->node[n];
+    const double w = task_w(task_lbk);
+    T->cnt->alg1_calls++;
+
+    /* line 3: task_prev <- Q^n[-1].  A node that never ran a task has a
+     * virtual predecessor that ends each stage exactly when the new task could
+     * start it ([R-1]); its a_[-1] is a itself ([R-9]). */
+    double prev_ef[MAXS];
+    if (nd->last_task >= 0) {
+        for (int s = 0; s < S; ++s) prev_ef[s] = T->path[nd->last_task].ef[s];
+    } else {
+        double v = a;
+        for (int s = 0; s < S; ++s) { prev_ef[s] = v; v = v + eta_f(T, n, s) * w; }
+    }
+
+    /* line 3: Q_temp <- Q_train^n (a copy; dequeue = advance the front). */
+    int64_t qlen = nd->q_len;
+    int64_t *qtemp = (int64_t *)malloc((size_t)(qlen > 0 ? qlen : 1) * sizeof(int64_t));
+    memcpy(qtemp, nd->q_train, (size_t)qlen * sizeof(int64_t));
+    int64_t front = 0;
+    int *remove = (int *)calloc((size_t)(qlen > 0 ? qlen : 1), sizeof(int));
+
+    double II = 0.0;                                   /* line 3 */
+    double end_prev_stage = a;                         /* end_f^0 := a ([R-2]) */
+    for (int s = 0; s < S; ++s) {                      /* line 4 */
+        T->cnt->stage_iters++;
+        const double dF = eta_f(T, n, s) * w;
+        double start = MAX(end_prev_stage, prev_ef[s]);  /* line 5 */
+        double end = start + dF;                          /* line 6 */
+        double offset = 0.0;                              /* line 7 */
+        while (front < qlen) {                            /* line 8 */
+            int64_t k = front;
+            int64_t tt = qtemp[front++];                  /* line 9: dequeue */
+            const path_t *pt = &T->path[tt];
+            if (end <= pt->sb[s]) {                       /* line 10 */
+                front--;                                  /* line 11: reinstated at the front ([R-3]) */
+                T->cnt->scan_break++;
+                break;                                    /* line 12 */
+            }
+            T->cnt->scan_consumed++;
+            start = MAX(start, pt->eb[s]);                /* line 13 */
+            end = start + dF;                             /* line 14 */
+            if (prev_ef[s] <= pt->sb[s]) {                /* line 15 */
+                offset = offset + eta_b(T, n, s) * task_w(T->lbk[tt]);   /* line 16 ([R-7]) */
+                T->cnt->offset_adds++;
+            }
+            if (s == 0 && pt->eb[0] <= now) {             /* line 17: CheckExecuted ([R-5]) */
+                /* line 18: remove from Q_train^n (index k of the original queue,
+                 * which Q_temp copied in order). */
+                remove[k] = 1;
+            }
+        }
+        II = II + ((start - prev_ef[s]) - offset);        /* line 19 ([R-8], grouping [R-II]) */
+        sf[s] = start;
+        ef[s] = end;
+        end_prev_stage = end;
+    }
+    *II_out = II;
+    *R_out = ef[S - 1] - a;                               /* line 20 */
+
+    /* apply line-18 removals to Q_train^n */
+    int64_t m = 0;
+    for (int64_t k = 0; k < qlen; ++k)
+        if (!remove[k]) nd->q_train[m++] = nd->q_train[k];
+    nd->q_len = m;
+    free(remove);
+    free(qtemp);
+}
+
+/* Eq. 1: IP = -max{ II/S - (a - a_[-1]), tau }. */
+static double idleness_profit(double II, int S, double a, double a_last, double tau)
+{
+    return -MAX(II / (double)S - (a - a_last), tau);
+}
+
+/* Eq. 2: LC = 1/(σ√(2π)) · exp{-(ℓ-μ)²/(2σ²)} with μ, σ the population mean
+ * and standard deviation of lengths previously run on the node ([R-10]);
+ * σ floored at sigma_floor, fewer than two samples -> lc0 ([R-11]).
+ * parity unpinned for lc0 (a reading, not a formula). */
+static double length_consistency(const trace_t *T, const node_t *nd, int l)
+{
+    const orc_params *P = T->par;
+    if (nd->hist_cnt < 2) { T->cnt->lc_cold++; return P->lc0; }
+    T->cnt->lc_exp++;
+    double mu = (double)nd->hist_sum / (double)nd->hist_cnt;
+    int64_t var_num = nd->hist_cnt * nd->hist_sumsq - nd->hist_sum * nd->hist_sum; /* cnt²·Var, exact */
+    double sigma = MAX(sqrt((double)var_num) / (double)nd->hist_cnt, P->sigma_floor);
+    double k = 0.5 / (sigma * sigma);                       /* 1/(2σ²) */
+    double c = 1.0 / (sigma * 0x1.40d931ff62705p+1);        /* 1/(σ√(2π)) */
+    double d = (double)l - mu;
+    return c * orc_exp_neg((d * d) * k);
+}
+
+/* Eq. 3: f = (IP + λ2·LC) / (λ1·R). */
+static double priority(const orc_params *P, double IP, double LC, double R)
+{
+    return (IP + P->lambda2 * LC) / (P->lambda1 * R);
+}
+
+/* tau_R for an inference task: slo_mult x its uncontended forward latency on
+ * node 0 ([R-16]) or a constant. */
+static double tau_R(const trace_t *T, uint32_t v)
+{
+    const orc_params *P = T->par;
+    if (P->slo_mode == 1) return P->slo_const;
+    double w = task_w(v);
+    double acc = 0.0;
+    for (int s = 0; s < T->S; ++s) acc = acc + eta_f(T, 0, s) * w;
+    return P->slo_mult * acc;
+}
+
+/* Eq. 4: defer the training task iff
+ *   min_n { max_{task in Q^n} end_f^S + η_F^n·C'ℓ'² } - a' > tau_R
+ * for the next enqueued inference task (a', ℓ', C') ([R-14], [R-15]). */
+static int should_deprioritize(trace_t *T, uint32_t next_lbk, double a_next)
+{
+    const int N = T->N, S = T->S;
+    T->cnt->eq4_checks++;
+    double w = task_w(next_lbk);
+    double m = INFINITY;
+    for (int n = 0; n < N; ++n) {
+        const node_t *nd = &T->node[n];
+        double latest = nd->has_efS ? nd->max_efS : -INFINITY;   /* max over empty Q^n */
+        double x = latest + eta_f(T, n, S - 1) * w;
+        m = MIN(m, x);
+    }
+    return (m - a_next) > tau_R(T, next_lbk);
+}
+
+/* Backward planning: immediately after the forward path,
+ * stages S..1 in reverse, each after the previous stage's backward and after
+ * every backward already planned on that GPU. */
+static void plan_backward(trace_t *T, int n, uint32_t v, path_t *p)
+{
+    const int S = T->S;
+    node_t *nd = &T->node[n];
+    double w = task_w(v);
+    double x = p->ef[S - 1];
+    for (int s = S - 1; s >= 0; --s) {
+        /* latest planned backward end on GPU (n, s).  Entries already removed
+         * from Q_train^n ended before `now`, which precedes x, so the queue
+         * holds every backward that can matter. */
+        double latest = -INFINITY;
+        for (int64_t k = 0; k < nd->q_len; ++k) latest = MAX(latest, T->path[nd->q_train[k]].eb[s]);
+        p->sb[s] = MAX(x, latest);
+        p->eb[s] = p->sb[s] + eta_b(T, n, s) * w;
+        x = p->eb[s];
+    }
+}
+
+int orc_run_trace(const orc_profile *prof, const orc_params *par,
+                  int64_t n_tasks, int64_t n_inf,
+                  const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
+                  uint32_t *node_defer, int32_t *decision_idx, double *completion,
+                  double *start_f1, double *paths, double *cand,
+                  orc_summary *summary, orc_counters *counters)
+{
+    const int N = prof->n_nodes, S = prof->n_stages;
+    orc_summary sm;
+    memset(&sm, 0, sizeof sm);
+    orc_counters dummy;
+    memset(&dummy, 0, sizeof dummy);
+    if (!counters) counters = &dummy;
+
+    const int64_t nI = n_inf, nT = n_tasks - n_inf;
+    sm.n_tasks = n_tasks; sm.n_inf = nI; sm.n_train = nT;
+
+    /* ---- input validation (inputs must be finite, ordered and in range) ---- */
+    int bad = (N < 1 || S < 1 || S > MAXS || nI < 0 || nT < 0 || par->qcap < 1 || !(par->lambda1 > 0.0));
+    for (int k = 0; k < N * S && !bad; ++k)
+        bad = !(prof->eta_f[k] > 0.0 && prof->eta_f[k] < INFINITY && prof->eta_b[k] > 0.0 && prof->eta_b[k] < INFINITY);
+    for (int64_t t = 0; t < n_tasks && !bad; ++t) {
+        uint32_t v = lbk[t];
+        bad = (v >> 21) != 0 || task_len(v) < 1 || task_len(v) > 2048 || task_batch(v) < 1 ||
+              task_kind(v) != (t >= nI) || !(arrival[t] >= 0.0 && arrival[t] < INFINITY) ||
+              (t > 0 && t < nI && arrival[t] < arrival[t - 1]) ||
+              (par->policy == ORC_FIXED && (fixed_node[t] < 0 || fixed_node[t] >= N));
+    }
+    if (!bad && par->policy == ORC_SEPARATE && N == 1 && nI > 0 && nT > 0) bad = 1;
+    if (bad) {
+        sm.status = ORC_EINVAL;
+        if (summary) *summary = sm;
+        return ORC_EINVAL;
+    }
+
+    trace_t T;
+    T.prof = prof; T.par = par; T.N = N; T.S = S;
+    T.arrival = arrival; T.lbk = lbk; T.cnt = counters;
+    T.path = (path_t *)calloc((size_t)(n_tasks > 0 ? n_tasks : 1), sizeof(path_t));
+    T.node = (node_t *)calloc((size_t)N, sizeof(node_t));
+    for (int n = 0; n < N; ++n) {
+        T.node[n].last_task = -1;
+        T.node[n].q_train = (int64_t *)malloc((size_t)par->qcap * sizeof(int64_t));
+    }
+    uint32_t *defer = (uint32_t *)calloc((size_t)(n_tasks > 0 ? n_tasks : 1), sizeof(uint32_t));
+
+    /* Separate's partition ([R-20]) */
+    int n_tr_nodes = 0, n_inf_nodes = N;
+    if (par->policy == ORC_SEPARATE && nI > 0 && nT > 0) {
+        n_tr_nodes = (int)floor((double)N * par->alpha + 0.5);
+        if (n_tr_nodes < 1) n_tr_nodes = 1;
+        if (n_tr_nodes > N - 1) n_tr_nodes = N - 1;
+        n_inf_nodes = N - n_tr_nodes;
+    }
+
+    /* ---- the global queue: inference by arrival, training released at the
+     * previous training task's S1 forward end ([R-18]) ---- */
+    int64_t i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0;
+    double r = (nT > 0) ? arrival[nI] : INFINITY;
+    double t_last = -INFINITY;
+    int status = ORC_OK;
+    double IIv[256], Rv[256], fv[256];
+    double (*sfv)[MAXS] = (double (*)[MAXS])malloc((size_t)N * sizeof(double[MAXS]));
+    double (*efv)[MAXS] = (double (*)[MAXS])malloc((size_t)N * sizeof(double[MAXS]));
+    double *IIa = N <= 256 ? IIv : (double *)malloc((size_t)N * sizeof(double));
+    double *Ra = N <= 256 ? Rv : (double *)malloc((size_t)N * sizeof(double));
+    double *fa = N <= 256 ? fv : (double *)malloc((size_t)N * sizeof(double));
+
+    while (i < nI || j < nT) {
+        if (++iters > 2 * (nI + nT) + 2) { status = ORC_EBUDGET; break; }
+        double t_inf = (i < nI) ? arrival[i] : INFINITY;
+        int64_t task;
+        double now;
+        if (t_inf <= r) {               /* ties: inference first ([R-19]) */
+            task = i; now = t_inf;
+        } else {
+            task = nI + j; now = r;
+            /* queue-level deprioritisation (Eq. 4) against the next enqueued
+             * inference task; the training task moves behind it ([R-15]). */
+            if (par->policy == ORC_LEMIX && par->deprioritize && i < nI &&
+                should_deprioritize(&T, lbk[i], arrival[i])) {
+                r = arrival[i];
+                defer[task]++;
+                counters->deferrals++;
+                sm.n_deferrals++;
+                continue;
+            }
+        }
+        const uint32_t v = lbk[task];
+        const int is_train = task_kind(v);
+        const double a = now;           /* dispatch time ([R-2]) */
+        path_t *p = &T.path[task];
+
+        /* ---- task-level node allocation ---- */
+        int best = 0;
+        for (int n = 0; n < N && cand; ++n) {
+            cand[(step * N + n) * 3 + 0] = NAN;
+            cand[(step * N + n) * 3 + 1] = NAN;
+            cand[(step * N + n) * 3 + 2] = NAN;
+        }
+        if (par->policy == ORC_LEMIX) {
+            for (int n = 0; n < N; ++n) {
+                compute_idleness(&T, n, v, a, now, &IIa[n], &Ra[n], sfv[n], efv[n]);
+                const node_t *nd = &T.node[n];
+                double a_last = (nd->last_task >= 0) ? nd->a_last : a;
+                double IP = idleness_profit(IIa[n], S, a, a_last, par->tau);
+                double LC = length_consistency(&T, nd, task_len(v));
+                fa[n] = priority(par, IP, LC, Ra[n]);
+                if (cand) {
+                    cand[(step * N + n) * 3 + 0] = IIa[n];
+                    cand[(step * N + n) * 3 + 1] = Ra[n];
+                    cand[(step * N + n) * 3 + 2] = fa[n];
+                }
+            }
+            /* highest f wins; ties -> lowest node index ([R-13]) */
+            best = 0;
+            for (int n = 1; n < N; ++n)
+                if (fa[n] > fa[best]) best = n;
+        } else {
+            if (par->policy == ORC_RR) {
+                best = (int)(rr % N); rr++;
+            } else if (par->policy == ORC_SEPARATE) {
+                if (n_tr_nodes == 0) {                                    /* one kind only */
+                    if (is_train) best = (int)(sep_t++ % N); else best = (int)(sep_i++ % N);
+                } else if (is_train) {
+                    best = n_inf_nodes + (int)(sep_t++ % n_tr_nodes);
+                } else {
+                    best = (int)(sep_i++ % n_inf_nodes);
+                }
+            } else {
+                best = fixed_node[task];
+            }
+            compute_idleness(&T, best, v, a, now, &IIa[best], &Ra[best], sfv[best], efv[best]);
+            if (cand) {
+                cand[(step * N + best) * 3 + 0] = IIa[best];
+                cand[(step * N + best) * 3 + 1] = Ra[best];
+                cand[(step * N + best) * 3 + 2] = NAN;
+            }
+        }
+
+        /* ---- commit: the task joins Q^best ---- */
+        node_t *nd = &T.node[best];
+        for (int s = 0; s < S; ++s) { p->sf[s] = sfv[best][s]; p->ef[s] = efv[best][s]; }
+        const double w = task_w(v);
+        for (int s = 0; s < S; ++s) nd->busy[s] = nd->busy[s] + eta_f(&T, best, s) * w;
+        double done;
+        if (is_train) {
+            if (nd->q_len >= par->qcap) { status = ORC_EQCAP; break; }
+            plan_backward(&T, best, v, p);
+            nd->q_train[nd->q_len++] = task;
+            if (nd->q_len > counters->max_qlen) counters->max_qlen = nd->q_len;
+            for (int s = 0; s < S; ++s) nd->busy[s] = nd->busy[s] + eta_b(&T, best, s) * w;
+            nd->n_train_on++;
+            counters->commits_train++;
+            done = p->eb[0];
+        } else {
+            done = p->ef[S - 1];
+            double ttft = p->ef[S - 1] - arrival[task];       /* TTFT = R from arrival */
+            sm.sum_ttft = sm.sum_ttft + ttft;
+            if (ttft <= tau_R(&T, v)) sm.n_slo_met++;
+            /* version-at-inference: training tasks on this node whose backward
+             * (stage 1) ended by this task's forward start. */
+            int64_t pending = 0;
+            for (int64_t k = 0; k < nd->q_len; ++k) {
+                counters->version_scan++;
+                if (T.path[nd->q_train[k]].eb[0] > p->sf[0]) pending++;
+            }
+            sm.sum_version += nd->n_train_on - pending;
+        }
+        nd->last_task = task;
+        nd->a_last = a;
+        if (!nd->has_efS || p->ef[S - 1] > nd->max_efS) nd->max_efS = p->ef[S - 1];
+        nd->has_efS = 1;
+        nd->hist_cnt += 1;
+        nd->hist_sum += task_len(v);
+        nd->hist_sumsq += (int64_t)task_len(v) * task_len(v);
+        t_last = MAX(t_last, done);
+
+        if (node_defer) node_defer[task] = (uint32_t)best | ((defer[task] > 0xFFFFu ? 0xFFFFu : defer[task]) << 16);
+        if (decision_idx) decision_idx[task] = (int32_t)step;
+        if (completion) completion[task] = done;
+        if (start_f1) start_f1[task] = p->sf[0];
+        if (paths)
+            for (int s = 0; s < S; ++s) {
+                paths[(task * S + s) * 4 + 0] = p->sf[s];
+                paths[(task * S + s) * 4 + 1] = p->ef[s];
+                paths[(task * S + s) * 4 + 2] = is_train ? p->sb[s] : 0.0;
+                paths[(task * S + s) * 4 + 3] = is_train ? p->eb[s] : 0.0;
+            }
+        step++;
+        counters->decisions++;
+        if (is_train) {
+            j++;
+            r = (j < nT) ? MAX(arrival[nI + j], p->ef[0]) : INFINITY;
+        } else {
+            i++;
+        }
+    }
+
+    if (status == ORC_OK) {
+        /* ---- per-trace metrics ---- */
+        double t_first = INFINITY;
+        if (nI > 0) t_first = MIN(t_first, arrival[0]);
+        if (nT > 0) t_first = MIN(t_first, arrival[nI]);
+        sm.makespan = (n_tasks > 0) ? t_last - t_first : 0.0;
+        sm.throughput = (sm.makespan > 0.0) ? (double)n_tasks / sm.makespan : 0.0;
+        sm.mean_ttft = (nI > 0) ? sm.sum_ttft / (double)nI : 0.0;
+        sm.slo_attainment = (nI > 0) ? (double)sm.n_slo_met / (double)nI : 1.0;
+        double U = 0.0, stds = 0.0;
+        for (int n = 0; n < N; ++n) {
+            for (int s = 0; s < S; ++s) U = U + T.node[n].busy[s];
+            if (T.node[n].hist_cnt > 0) {
+                const node_t *q = &T.node[n];
+                sm.active_nodes++;
+                int64_t var_num = q->hist_cnt * q->hist_sumsq - q->hist_sum * q->hist_sum;
+                stds = stds + sqrt((double)var_num) / (double)q->hist_cnt;
+            }
+        }
+        sm.mean_util = (sm.makespan > 0.0) ? U / ((double)(N * S) * sm.makespan) : 0.0;
+        sm.mean_len_std = (sm.active_nodes > 0) ? stds / (double)sm.active_nodes : 0.0;
+    } else {
+        orc_summary e;
+        memset(&e, 0, sizeof e);
+        e.n_tasks = n_tasks; e.n_inf = nI; e.n_train = nT;
+        sm = e;
+    }
+    sm.status = status;
+    if (summary) *summary = sm;
+
+    if (IIa != IIv) { free(IIa); free(Ra); free(fa); }
+    free(sfv); free(efv);
+    for (int n = 0; n < N; ++n) free(T.node[n].q_train);
+    free(T.node); free(T.path); free(defer);
+    return status;
+}
+
+int orc_run_batch(const orc_profile *prof, const orc_params *par,
+                  int64_t n_traces, const int64_t *offsets, const int32_t *n_inf,
+                  const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
+                  uint32_t *node_defer, int32_t *decision_idx, double *completion,
+                  double *start_f1, orc_summary *summaries, orc_counters *counters)
+{
+    int first_err = ORC_OK;
+    for (int64_t t = 0; t < n_traces; ++t) {
+        int64_t o = offsets[t], n = offsets[t + 1] - offsets[t];
+        int st = orc_run_trace(prof, par, n, n_inf[t], arrival + o, lbk + o,
+                               fixed_node ? fixed_node + o : NULL,
+                               node_defer ? node_defer + o : NULL,
+                               decision_idx ? decision_idx + o : NULL,
+                               completion ? completion + o : NULL,
+                               start_f1 ? start_f1 + o : NULL, NULL, NULL,
+                               summaries ? summaries + t : NULL, counters);
+        if (st != ORC_OK && first_err == ORC_OK) first_err = st;
+    }
+    return first_err;
+}
