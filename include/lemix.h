@@ -1,0 +1,212 @@
+/*
+ * lemix.h -- C ABI of the B200-native LeMix placement-step library (liblemix.so).
+ *
+ * What it computes (arXiv 2507.21276, /root/reference/PAPER.md):
+ *   For every decision of a discrete-event loop over independent synthetic
+ *   traces, the pending task (an inference request or a training micro-batch)
+ *   is planned on every node with Algorithm 1 ComputeIdleness (PAPER.md:432-476,
+ *   §4.2) giving the idleness increase II and response time R, scored with
+ *   Eq. 1 (idleness profit), Eq. 2 (length consistency,
+ *   PAPER.md:555) and Eq. 3 (node priority f), and committed to
+ *   the node with the highest f; training tasks are first
+ *   checked against Eq. 4 queue-level deprioritisation.  The
+ *   Separate / NaiveMix (round-robin) baselines and a fixed
+ *   assignment run the same planner on their chosen node.  The exact
+ *   semantics, the readings of garbled passages and the canonical fp64
+ *   expression forms are in DESIGN.md; results are bit-identical to the CPU
+ *   oracle in oracle/.
+ *
+ * Conventions
+ *   - Ownership: the caller owns every buffer it passes.  lmx_load_* copy what
+ *     they need unless stated otherwise; outputs are copied into
+ *     caller-allocated arrays.
+ *   - Sequencing: create -> load_profile -> load_traces -> set_params -> run
+ *     -> sync -> get_*.  Profile/traces/params may be re-loaded between runs.
+ *     A call out of order returns LMX_ESTATE.
+ *   - Errors: every call returns an lmx_status; lmx_last_error() gives a
+ *     message naming the offending field, trace and task index.
+ *   - Asynchrony: lmx_run enqueues on the context's CUDA stream and returns;
+ *     lmx_sync waits and returns the first per-trace error (LMX_OK if none).
+ *   - Determinism: outputs are a pure function of (profile, traces, params);
+ *     they do not depend on the launch geometry, the GPU count or the order
+ *     in which traces are scheduled on the device.
+ *   - Not thread-safe: one context per thread / GPU.
+ */
+#ifndef LEMIX_H
+#define LEMIX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lmx_ctx lmx_ctx;   /* opaque; owns device buffers on one GPU */
+
+typedef enum {
+    LMX_OK = 0,
+    LMX_EINVAL = 1,   /* invalid argument or input data (field/trace/task in lmx_last_error) */
+    LMX_ESTATE = 2,   /* call out of sequence */
+    LMX_ENOMEM = 3,   /* device or pinned allocation failed */
+    LMX_ECUDA = 4,    /* CUDA runtime error */
+    LMX_ENCCL = 5,    /* NCCL unavailable or failed */
+    LMX_EQCAP = 6,    /* per trace: a node's training queue Q_train^n exceeded params.qcap */
+    LMX_EBUDGET = 7   /* per trace: decision budget exhausted (cannot happen for valid input) */
+} lmx_status;
+
+typedef enum { LMX_LEMIX = 0, LMX_RR = 1, LMX_SEPARATE = 2, LMX_FIXED = 3 } lmx_policy;
+typedef enum { LMX_HOST = 0, LMX_DEVICE = 1 } lmx_mem;
+
+/* Profile table (offline profiling, §4.1): stage latencies
+ * Δ_F = eta_f·C·ℓ², Δ_B = eta_b·C·ℓ².  Host memory, node-major
+ * [n_nodes * n_stages], every value finite and > 0.  1 <= n_nodes <= 128,
+ * 1 <= n_stages <= 16.  Copied. */
+typedef struct {
+    int32_t n_nodes;
+    int32_t n_stages;
+    const double *eta_f;
+    const double *eta_b;
+} lmx_profile;
+
+/* Task packing of len_batch_kind: query length ℓ in bits 0-11 (1..2048),
+ * batch size C in bits 12-19 (1..255), kind in bit 20 (0 inference,
+ * 1 training), bits 21-31 zero. */
+#define LMX_PACK(l, C, kind) ((uint32_t)(l) | ((uint32_t)(C) << 12) | ((uint32_t)(kind) << 20))
+
+/* A CSR batch of independent traces.
+ *   offsets[n_traces+1] (HOST memory): trace t owns tasks [offsets[t], offsets[t+1]),
+ *     offsets[0] == 0, non-decreasing, at most 2^19 tasks per trace.
+ *   n_inf[n_traces] (HOST memory): the first n_inf[t] tasks of trace t are
+ *     inference tasks in non-decreasing arrival order, the rest are training
+ *     tasks in release order.
+ *   arrival[n_tasks]: inference arrival time, or a training task's earliest
+ *     release a_min (seconds, finite, >= 0).
+ *   len_batch_kind[n_tasks]: LMX_PACK; the kind bit must match the position.
+ *   fixed_node[n_tasks]: node per task for LMX_FIXED, else may be NULL.
+ * The task arrays live in the memory named by the lmx_mem argument of
+ * lmx_load_traces.  Per-task field errors are detected on the device during
+ * lmx_run and reported per trace (status LMX_EINVAL). */
+typedef struct {
+    int64_t n_traces;
+    const int64_t *offsets;
+    const int32_t *n_inf;
+    const double *arrival;
+    const uint32_t *len_batch_kind;
+    const int32_t *fixed_node;
+} lmx_traces;
+
+/* Scheduler parameters.  lmx_params_default() fills the DESIGN.md defaults:
+ * LeMix, λ1 = λ2 = 1, τ = 0, slo_mult = 5, σ_floor = 1,
+ * lc0 = 0, α = 0.5, deprioritise on, per-task τ_R, qcap = 512. */
+typedef struct {
+    int32_t policy;        /* lmx_policy */
+    int32_t deprioritize;  /* 1: Eq. 4 on (LeMix only); 0: the "w/o prioritize" ablation */
+    int32_t slo_mode;      /* 0: τ_R = slo_mult · Σ_s η_F^{0,s}·C·ℓ²; 1: τ_R = slo_const */
+    int32_t qcap;          /* capacity of each Q_train^n (1..65536); overflow -> LMX_EQCAP */
+    double lambda1;        /* Eq. 3, > 0 */
+    double lambda2;        /* Eq. 3, >= 0 */
+    double tau;            /* Eq. 1 threshold */
+    double slo_mult;       /* >= 0 */
+    double slo_const;      /* seconds, slo_mode 1 */
+    double sigma_floor;    /* Eq. 2 σ floor, > 0 */
+    double lc0;            /* Eq. 2 value for nodes with < 2 tasks of history */
+    double alpha;          /* Separate: N_train = clamp(floor(N·α + 0.5), 1, N-1), α in [0, 1] */
+} lmx_params;
+
+/* Per-trace summary (metrics of PAPER.md:786-790).  For a trace whose status
+ * is not LMX_OK only n_tasks, n_inf, n_train and status are set. */
+typedef struct {
+    int64_t n_tasks, n_inf, n_train;
+    int64_t n_slo_met;      /* inference tasks with TTFT <= τ_R */
+    int64_t n_deferrals;    /* Eq. 4 deferrals */
+    int64_t active_nodes;   /* nodes that ran >= 1 task (consolidation) */
+    int64_t sum_version;    /* Σ over inference tasks of the node's completed-training count */
+    int64_t status;         /* lmx_status of this trace */
+    double makespan;        /* last completion - first arrival */
+    double throughput;      /* tasks / makespan */
+    double sum_ttft, mean_ttft;
+    double slo_attainment;  /* n_slo_met / n_inf (1.0 when n_inf == 0) */
+    double mean_util;       /* Σ busy / (N·S·makespan) */
+    double mean_len_std;    /* mean over active nodes of the population σ of lengths */
+} lmx_summary;
+
+/* Aggregate of the per-trace summaries of one cell (e.g. one (rate, policy)
+ * point of a sweep); the "sum_*" fields add the per-trace value over the
+ * cell's LMX_OK traces.  Reduced across ranks by lmx_allreduce_cells. */
+typedef struct {
+    int64_t n_traces, n_failed, n_tasks, n_inf, n_train, n_slo_met, n_deferrals,
+            sum_active_nodes, sum_version;
+    double sum_makespan, sum_throughput, sum_ttft, sum_mean_ttft, sum_slo_attainment,
+           sum_mean_util, sum_mean_len_std;
+} lmx_cell_summary;
+
+#define LMX_CELL_NI 9
+#define LMX_CELL_NF 7
+
+void lmx_params_default(lmx_params *p);
+
+/* Create a context on CUDA device `device`; work is enqueued on `cuda_stream`
+ * (a cudaStream_t, NULL = a stream owned by the context). */
+lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream);
+void lmx_destroy(lmx_ctx *ctx);
+const char *lmx_last_error(const lmx_ctx *ctx);
+
+lmx_status lmx_load_profile(lmx_ctx *ctx, const lmx_profile *profile);
+
+/* HOST: task arrays are copied to device buffers owned by the context
+ * (asynchronously on the context stream when the host memory is pinned).
+ * DEVICE: the task arrays are borrowed device pointers and must stay valid
+ * until the next lmx_sync.  offsets and n_inf are always host memory. */
+lmx_status lmx_load_traces(lmx_ctx *ctx, const lmx_traces *traces, lmx_mem mem);
+
+lmx_status lmx_set_params(lmx_ctx *ctx, const lmx_params *params);
+
+/* Optional: group traces into cells for lmx_get_cells (host memory,
+ * cell_of_trace[n_traces] in [0, n_cells)).  NULL / 1 = one cell. */
+lmx_status lmx_set_cells(lmx_ctx *ctx, const int32_t *cell_of_trace, int32_t n_cells);
+
+/* Optional: keep per-task outputs (default on).  Off = summary-only runs. */
+lmx_status lmx_set_outputs(lmx_ctx *ctx, int per_task);
+
+/* Run every trace (one persistent kernel) and reduce per-cell summaries. */
+lmx_status lmx_run(lmx_ctx *ctx);
+lmx_status lmx_sync(lmx_ctx *ctx);
+
+/* Per-task outputs, indexed like the task arrays.  node_defer = node index
+ * (bits 0-15) | Eq. 4 deferral count saturated at 0xFFFF (bits 16-31);
+ * decision_idx = the decision (0-based, per trace) that placed the task;
+ * completion = inference end_f^S, training end_b^1; start_f1 = start_f^1.
+ * Any pointer may be NULL.  `mem` says where the destination lives. */
+lmx_status lmx_get_assignments(lmx_ctx *ctx, uint32_t *node_defer, int32_t *decision_idx, lmx_mem mem);
+lmx_status lmx_get_times(lmx_ctx *ctx, double *completion, double *start_f1, lmx_mem mem);
+
+/* Per-trace summaries [n_traces] (host memory). */
+lmx_status lmx_get_summaries(lmx_ctx *ctx, lmx_summary *per_trace);
+/* Per-cell aggregates [n_cells] (host memory). */
+lmx_status lmx_get_cells(lmx_ctx *ctx, lmx_cell_summary *cells);
+
+/* Multi-GPU: one grouped ncclAllReduce(sum) of the cell aggregates over
+ * `nccl_comm` (an ncclComm_t) on the context stream.  NCCL is resolved at run
+ * time (dlopen "libnccl.so.2"); LMX_ENCCL if unavailable. */
+lmx_status lmx_allreduce_cells(lmx_ctx *ctx, void *nccl_comm);
+/* Helpers to build a communicator without a framework: rank 0 calls
+ * lmx_nccl_unique_id, ships the 128 bytes to every rank, each calls
+ * lmx_nccl_comm_init on its own device. */
+lmx_status lmx_nccl_unique_id(void *id128);
+lmx_status lmx_nccl_comm_init(void **comm, int nranks, const void *id128, int rank, int device);
+lmx_status lmx_nccl_comm_destroy(void *comm);
+
+/* Device time of the last run's event-loop kernel (CUDA events on the context
+ * stream; valid after lmx_sync) and the number of kernels the library
+ * launched in that run. */
+lmx_status lmx_get_timing(lmx_ctx *ctx, float *kernel_ms, float *run_ms, int32_t *launches);
+
+/* Launch geometry chosen for the last run (for reports). */
+lmx_status lmx_get_geometry(lmx_ctx *ctx, int32_t *grid, int32_t *block, int32_t *lanes_per_trace,
+                            int32_t *smem_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LEMIX_H */

@@ -1,0 +1,682 @@
+// lemix_api.cpp -- host side of the liblemix C ABI (include/lemix.h).
+//
+// Owns device memory, validates what can be validated on the host (profile,
+// parameters, CSR metadata), launches the persistent event-loop kernel and the
+// cell reduction on the context stream, and resolves NCCL at run time for the
+// one cross-GPU summary all-reduce.  No scheduling arithmetic happens here.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lemix.h"
+#include "lemix_internal.h"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    bool owned = true;
+    ~DevBuf() { release(); }
+    void release()
+    {
+        if (p && owned) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+        owned = true;
+    }
+    cudaError_t ensure(size_t b)
+    {
+        if (owned && p && bytes >= b) return cudaSuccess;
+        release();
+        if (b == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, b);
+        if (e == cudaSuccess) bytes = b;
+        else p = nullptr;
+        return e;
+    }
+    void borrow(const void *q)
+    {
+        release();
+        p = const_cast<void *>(q);
+        owned = false;
+    }
+};
+
+bool is_pinned(const void *h)
+{
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+const char *field_name(int code)
+{
+    switch (code) {
+    case lmx::kErrLen: return "len_batch_kind.length (must be 1..2048)";
+    case lmx::kErrBatch: return "len_batch_kind.batch (must be 1..255)";
+    case lmx::kErrKind: return "len_batch_kind.kind (must match the inference-first layout)";
+    case lmx::kErrBits: return "len_batch_kind (bits 21-31 must be zero)";
+    case lmx::kErrArrival: return "arrival (must be finite and >= 0)";
+    case lmx::kErrOrder: return "arrival (inference tasks must be non-decreasing)";
+    case lmx::kErrFixed: return "fixed_node (must be in [0, n_nodes))";
+    case lmx::kErrSeparateN1: return "policy Separate needs n_nodes >= 2 when both kinds are present";
+    default: return "unknown";
+    }
+}
+
+// ---- NCCL, resolved at run time (the process may already have torch's copy) ----
+typedef int (*nccl_get_unique_id_t)(void *);
+typedef int (*nccl_comm_init_rank_t)(void **, int, /*ncclUniqueId by value*/ struct NcclId128, int);
+struct NcclId128 { char internal[128]; };
+typedef int (*nccl_comm_init_rank2_t)(void **, int, NcclId128, int);
+typedef int (*nccl_all_reduce_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+typedef int (*nccl_group_t)();
+typedef int (*nccl_comm_destroy_t)(void *);
+
+struct Nccl {
+    void *h = nullptr;
+    nccl_get_unique_id_t get_unique_id = nullptr;
+    nccl_comm_init_rank2_t comm_init_rank = nullptr;
+    nccl_all_reduce_t all_reduce = nullptr;
+    nccl_group_t group_start = nullptr, group_end = nullptr;
+    nccl_comm_destroy_t comm_destroy = nullptr;
+    bool load()
+    {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        get_unique_id = (nccl_get_unique_id_t)dlsym(h, "ncclGetUniqueId");
+        comm_init_rank = (nccl_comm_init_rank2_t)dlsym(h, "ncclCommInitRank");
+        all_reduce = (nccl_all_reduce_t)dlsym(h, "ncclAllReduce");
+        group_start = (nccl_group_t)dlsym(h, "ncclGroupStart");
+        group_end = (nccl_group_t)dlsym(h, "ncclGroupEnd");
+        comm_destroy = (nccl_comm_destroy_t)dlsym(h, "ncclCommDestroy");
+        return get_unique_id && comm_init_rank && all_reduce && group_start && group_end && comm_destroy;
+    }
+};
+Nccl g_nccl;
+// ncclDataType_t / ncclRedOp_t values (stable NCCL ABI)
+constexpr int kNcclInt64 = 4, kNcclFloat64 = 8, kNcclSum = 0;
+
+}  // namespace
+
+struct lmx_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+
+    // profile
+    bool have_profile = false;
+    int N = 0, S = 0;
+    DevBuf eta;
+
+    // traces
+    bool have_traces = false;
+    int64_t n_traces = 0, n_tasks = 0;
+    std::vector<int64_t> h_offsets;
+    std::vector<int32_t> h_n_inf;
+    bool has_fixed = false;
+    DevBuf offsets, n_inf, arrival, lbk, fixed;
+
+    // params
+    bool have_params = false;
+    lmx_params par{};
+
+    // cells
+    int32_t n_cells = 1;
+    DevBuf cell_of, cell_i, cell_f;
+    bool cells_set = false;
+
+    // outputs / state
+    int per_task = 1;
+    DevBuf node_defer, decision_idx, completion, start_f1;
+    DevBuf summaries, trace_err, work, first_bad, ring_be, ring_w;
+    bool ran = false, synced = false;
+
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
+    int32_t launches = 0, grid = 0, block = 0, lanes = 0, smem = 0;
+
+    lmx_status fail(lmx_status s, const std::string &m)
+    {
+        err = m;
+        return s;
+    }
+    lmx_status cuda(cudaError_t e, const char *what)
+    {
+        if (e == cudaSuccess) return LMX_OK;
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        return LMX_ECUDA;
+    }
+};
+
+extern "C" {
+
+void lmx_params_default(lmx_params *p)
+{
+    if (!p) return;
+    p->policy = LMX_LEMIX;
+    p->deprioritize = 1;
+    p->slo_mode = 0;
+    p->qcap = 512;
+    p->lambda1 = 1.0;
+    p->lambda2 = 1.0;
+    p->tau = 0.0;
+    p->slo_mult = 5.0;
+    p->slo_const = 0.0;
+    p->sigma_floor = 1.0;
+    p->lc0 = 0.0;
+    p->alpha = 0.5;
+}
+
+lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
+{
+    if (!out) {
+        g_create_error = "lmx_create: out is NULL";
+        return LMX_EINVAL;
+    }
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || device < 0 || device >= n) {
+        g_create_error = std::string("lmx_create: no CUDA device ") + std::to_string(device) +
+                         (e != cudaSuccess ? std::string(" (") + cudaGetErrorString(e) + ")" : "");
+        cudaGetLastError();
+        return LMX_ECUDA;
+    }
+    if ((e = cudaSetDevice(device)) != cudaSuccess) {
+        g_create_error = std::string("cudaSetDevice: ") + cudaGetErrorString(e);
+        return LMX_ECUDA;
+    }
+    lmx_ctx *c = new lmx_ctx();
+    c->device = device;
+    if (cuda_stream) {
+        c->stream = (cudaStream_t)cuda_stream;
+    } else {
+        if ((e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+            g_create_error = std::string("cudaStreamCreate: ") + cudaGetErrorString(e);
+            delete c;
+            return LMX_ECUDA;
+        }
+        c->own_stream = true;
+    }
+    cudaEventCreate(&c->ev0);
+    cudaEventCreate(&c->ev1);
+    cudaEventCreate(&c->ev2);
+    lmx_params_default(&c->par);
+    if (c->work.ensure(8) != cudaSuccess || c->first_bad.ensure(8) != cudaSuccess) {
+        g_create_error = "lmx_create: device allocation failed";
+        delete c;
+        return LMX_ENOMEM;
+    }
+    *out = c;
+    return LMX_OK;
+}
+
+void lmx_destroy(lmx_ctx *c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev2) cudaEventDestroy(c->ev2);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char *lmx_last_error(const lmx_ctx *c) { return c ? c->err.c_str() : g_create_error.c_str(); }
+
+lmx_status lmx_load_profile(lmx_ctx *c, const lmx_profile *pr)
+{
+    if (!c) return LMX_EINVAL;
+    if (!pr || !pr->eta_f || !pr->eta_b) return c->fail(LMX_EINVAL, "lmx_load_profile: NULL profile or table");
+    if (pr->n_nodes < 1 || pr->n_nodes > 128)
+        return c->fail(LMX_EINVAL, "profile.n_nodes must be in [1, 128], got " + std::to_string(pr->n_nodes));
+    if (pr->n_stages < 1 || pr->n_stages > 16)
+        return c->fail(LMX_EINVAL, "profile.n_stages must be in [1, 16], got " + std::to_string(pr->n_stages));
+    const int NS = pr->n_nodes * pr->n_stages;
+    std::vector<double> h(2 * (size_t)NS);
+    for (int k = 0; k < NS; ++k) {
+        const double f = pr->eta_f[k], b = pr->eta_b[k];
+        if (!(f > 0.0 && std::isfinite(f)))
+            return c->fail(LMX_EINVAL, "profile.eta_f[" + std::to_string(k) + "] must be finite and > 0");
+        if (!(b > 0.0 && std::isfinite(b)))
+            return c->fail(LMX_EINVAL, "profile.eta_b[" + std::to_string(k) + "] must be finite and > 0");
+        h[k] = f;
+        h[NS + k] = b;
+    }
+    cudaSetDevice(c->device);
+    if (c->eta.ensure(h.size() * sizeof(double)) != cudaSuccess) return c->fail(LMX_ENOMEM, "profile allocation");
+    lmx_status s = c->cuda(cudaMemcpyAsync(c->eta.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                           c->stream),
+                           "profile copy");
+    if (s != LMX_OK) return s;
+    s = c->cuda(cudaStreamSynchronize(c->stream), "profile copy");
+    if (s != LMX_OK) return s;
+    c->N = pr->n_nodes;
+    c->S = pr->n_stages;
+    c->have_profile = true;
+    c->ran = false;
+    return LMX_OK;
+}
+
+lmx_status lmx_load_traces(lmx_ctx *c, const lmx_traces *tr, lmx_mem mem)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->have_profile) return c->fail(LMX_ESTATE, "lmx_load_traces: load the profile first");
+    if (!tr || !tr->offsets || !tr->n_inf) return c->fail(LMX_EINVAL, "lmx_load_traces: NULL traces/offsets/n_inf");
+    if (tr->n_traces < 0) return c->fail(LMX_EINVAL, "traces.n_traces must be >= 0");
+    if (mem != LMX_HOST && mem != LMX_DEVICE) return c->fail(LMX_EINVAL, "lmx_load_traces: bad lmx_mem");
+    const int64_t T = tr->n_traces;
+    if (tr->offsets[0] != 0) return c->fail(LMX_EINVAL, "traces.offsets[0] must be 0");
+    for (int64_t t = 0; t < T; ++t) {
+        const int64_t len = tr->offsets[t + 1] - tr->offsets[t];
+        if (len < 0) return c->fail(LMX_EINVAL, "traces.offsets must be non-decreasing (trace " + std::to_string(t) + ")");
+        if (len > (int64_t(1) << 19))
+            return c->fail(LMX_EINVAL, "trace " + std::to_string(t) + " has more than 2^19 tasks");
+        if (tr->n_inf[t] < 0 || tr->n_inf[t] > len)
+            return c->fail(LMX_EINVAL, "traces.n_inf[" + std::to_string(t) + "] must be in [0, trace length]");
+    }
+    const int64_t M = tr->offsets[T];
+    if (M > 0 && (!tr->arrival || !tr->len_batch_kind))
+        return c->fail(LMX_EINVAL, "traces.arrival / len_batch_kind are NULL");
+    cudaSetDevice(c->device);
+    c->h_offsets.assign(tr->offsets, tr->offsets + T + 1);
+    c->h_n_inf.assign(tr->n_inf, tr->n_inf + T);
+    if (c->offsets.ensure((T + 1) * 8) != cudaSuccess || c->n_inf.ensure(std::max<int64_t>(T, 1) * 4) != cudaSuccess)
+        return c->fail(LMX_ENOMEM, "trace metadata allocation");
+    lmx_status s = c->cuda(cudaMemcpyAsync(c->offsets.p, c->h_offsets.data(), (T + 1) * 8, cudaMemcpyHostToDevice,
+                                           c->stream), "offsets copy");
+    if (s == LMX_OK && T > 0)
+        s = c->cuda(cudaMemcpyAsync(c->n_inf.p, c->h_n_inf.data(), T * 4, cudaMemcpyHostToDevice, c->stream),
+                    "n_inf copy");
+    if (s != LMX_OK) return s;
+    c->has_fixed = tr->fixed_node != nullptr;
+    if (mem == LMX_DEVICE) {
+        c->arrival.borrow(tr->arrival);
+        c->lbk.borrow(tr->len_batch_kind);
+        if (c->has_fixed) c->fixed.borrow(tr->fixed_node);
+    } else {
+        if (c->arrival.ensure(std::max<int64_t>(M, 1) * 8) != cudaSuccess ||
+            c->lbk.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess ||
+            (c->has_fixed && c->fixed.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess))
+            return c->fail(LMX_ENOMEM, "trace buffers allocation (" + std::to_string(M) + " tasks)");
+        if (M > 0) {
+            s = c->cuda(cudaMemcpyAsync(c->arrival.p, tr->arrival, M * 8, cudaMemcpyHostToDevice, c->stream),
+                        "arrival copy");
+            if (s == LMX_OK)
+                s = c->cuda(cudaMemcpyAsync(c->lbk.p, tr->len_batch_kind, M * 4, cudaMemcpyHostToDevice, c->stream),
+                            "len_batch_kind copy");
+            if (s == LMX_OK && c->has_fixed)
+                s = c->cuda(cudaMemcpyAsync(c->fixed.p, tr->fixed_node, M * 4, cudaMemcpyHostToDevice, c->stream),
+                            "fixed_node copy");
+            if (s != LMX_OK) return s;
+        }
+        (void)is_pinned;
+    }
+    c->n_traces = T;
+    c->n_tasks = M;
+    c->have_traces = true;
+    c->ran = false;
+    if (!c->cells_set) c->n_cells = 1;
+    return LMX_OK;
+}
+
+lmx_status lmx_set_params(lmx_ctx *c, const lmx_params *p)
+{
+    if (!c) return LMX_EINVAL;
+    if (!p) return c->fail(LMX_EINVAL, "lmx_set_params: NULL params");
+    if (p->policy < LMX_LEMIX || p->policy > LMX_FIXED) return c->fail(LMX_EINVAL, "params.policy out of range");
+    if (p->deprioritize != 0 && p->deprioritize != 1) return c->fail(LMX_EINVAL, "params.deprioritize must be 0 or 1");
+    if (p->slo_mode != 0 && p->slo_mode != 1) return c->fail(LMX_EINVAL, "params.slo_mode must be 0 or 1");
+    if (p->qcap < 1 || p->qcap > 65536) return c->fail(LMX_EINVAL, "params.qcap must be in [1, 65536]");
+    if (!(p->lambda1 > 0.0 && std::isfinite(p->lambda1))) return c->fail(LMX_EINVAL, "params.lambda1 must be finite and > 0");
+    if (!(p->lambda2 >= 0.0 && std::isfinite(p->lambda2))) return c->fail(LMX_EINVAL, "params.lambda2 must be finite and >= 0");
+    if (!std::isfinite(p->tau)) return c->fail(LMX_EINVAL, "params.tau must be finite");
+    if (!(p->slo_mult >= 0.0 && std::isfinite(p->slo_mult))) return c->fail(LMX_EINVAL, "params.slo_mult must be finite and >= 0");
+    if (!std::isfinite(p->slo_const)) return c->fail(LMX_EINVAL, "params.slo_const must be finite");
+    if (!(p->sigma_floor > 0.0 && std::isfinite(p->sigma_floor))) return c->fail(LMX_EINVAL, "params.sigma_floor must be finite and > 0");
+    if (!std::isfinite(p->lc0)) return c->fail(LMX_EINVAL, "params.lc0 must be finite");
+    if (!(p->alpha >= 0.0 && p->alpha <= 1.0)) return c->fail(LMX_EINVAL, "params.alpha must be in [0, 1]");
+    c->par = *p;
+    c->have_params = true;
+    c->ran = false;
+    return LMX_OK;
+}
+
+lmx_status lmx_set_cells(lmx_ctx *c, const int32_t *cell_of, int32_t n_cells)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->have_traces) return c->fail(LMX_ESTATE, "lmx_set_cells: load traces first");
+    if (!cell_of || n_cells <= 1) {
+        c->n_cells = 1;
+        c->cells_set = false;
+        c->cell_of.release();
+        return LMX_OK;
+    }
+    if (n_cells > 65536) return c->fail(LMX_EINVAL, "n_cells must be <= 65536");
+    for (int64_t t = 0; t < c->n_traces; ++t)
+        if (cell_of[t] < 0 || cell_of[t] >= n_cells)
+            return c->fail(LMX_EINVAL, "cell_of_trace[" + std::to_string(t) + "] out of range");
+    cudaSetDevice(c->device);
+    if (c->cell_of.ensure(std::max<int64_t>(c->n_traces, 1) * 4) != cudaSuccess) return c->fail(LMX_ENOMEM, "cells");
+    lmx_status s = c->cuda(cudaMemcpyAsync(c->cell_of.p, cell_of, c->n_traces * 4, cudaMemcpyHostToDevice, c->stream),
+                           "cells copy");
+    if (s != LMX_OK) return s;
+    s = c->cuda(cudaStreamSynchronize(c->stream), "cells copy");
+    if (s != LMX_OK) return s;
+    c->n_cells = n_cells;
+    c->cells_set = true;
+    return LMX_OK;
+}
+
+lmx_status lmx_set_outputs(lmx_ctx *c, int per_task)
+{
+    if (!c) return LMX_EINVAL;
+    c->per_task = per_task ? 1 : 0;
+    return LMX_OK;
+}
+
+lmx_status lmx_run(lmx_ctx *c)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->have_profile || !c->have_traces || !c->have_params)
+        return c->fail(LMX_ESTATE, "lmx_run: load profile, traces and params first");
+    const lmx_params &P = c->par;
+    if (P.policy == LMX_FIXED && !c->has_fixed)
+        return c->fail(LMX_EINVAL, "policy LMX_FIXED needs traces.fixed_node");
+    cudaSetDevice(c->device);
+    const int64_t T = c->n_traces, M = c->n_tasks;
+
+    lmx::KParams k{};
+    k.N = c->N;
+    k.S = c->S;
+    int Tl = 1;
+    while (Tl < c->N && Tl < 32) Tl <<= 1;
+    k.T = Tl;
+    k.log2T = 0;
+    while ((1 << k.log2T) < Tl) k.log2T++;
+    k.npl = (c->N + Tl - 1) / Tl;
+    k.npad = lmx::npl_bucket(k.npl) * Tl;
+    k.policy = P.policy;
+    k.deprioritize = P.deprioritize;
+    k.slo_mode = P.slo_mode;
+    k.qcap = P.qcap;
+    int K = 1;
+    while (K < P.qcap) K <<= 1;
+    k.kmask = K - 1;
+    {
+        // Separate's training partition, PAPER.md:795 (host fp64, no contraction)
+        const double raw = std::floor((double)c->N * P.alpha + 0.5);
+        int ntr = (int)raw;
+        if (ntr < 1) ntr = 1;
+        if (ntr > c->N - 1) ntr = c->N - 1;
+        k.n_tr_sep = ntr < 1 ? 1 : ntr;
+    }
+    k.s_pow2 = (c->S & (c->S - 1)) == 0;
+    k.inv_S = 1.0 / (double)c->S;
+    k.lambda1 = P.lambda1;
+    k.lambda2 = P.lambda2;
+    k.tau = P.tau;
+    k.slo_mult = P.slo_mult;
+    k.slo_const = P.slo_const;
+    k.sigma_floor = P.sigma_floor;
+    k.lc0 = P.lc0;
+    k.n_traces = T;
+    k.offsets = (const int64_t *)c->offsets.p;
+    k.n_inf = (const int32_t *)c->n_inf.p;
+    k.arrival = (const double *)c->arrival.p;
+    k.lbk = (const uint32_t *)c->lbk.p;
+    k.fixed = c->has_fixed ? (const int32_t *)c->fixed.p : nullptr;
+    k.eta = (const double *)c->eta.p;
+
+    // geometry: persistent grid = resident CTAs, capped by the number of traces
+    int occ_err = 0;
+    const int per_sm = lmx::event_loop_occupancy(k, &occ_err);
+    if (occ_err != 0 || per_sm < 1)
+        return c->fail(LMX_ECUDA, std::string("event loop occupancy query failed: ") +
+                                      cudaGetErrorString((cudaError_t)occ_err));
+    int n_sm = 0;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
+    const int block = lmx::event_loop_block_threads();
+    const int tiles_per_block = block / Tl;
+    int64_t grid = (int64_t)n_sm * per_sm;
+    const int64_t need = (T + tiles_per_block - 1) / tiles_per_block;
+    grid = std::max<int64_t>(1, std::min(grid, need));
+    const int64_t tiles = grid * tiles_per_block;
+
+    // device buffers
+    const size_t ring_entries = (size_t)tiles * k.npad * K;
+    if (c->ring_be.ensure(ring_entries * c->S * sizeof(double2)) != cudaSuccess ||
+        c->ring_w.ensure(ring_entries * sizeof(double)) != cudaSuccess)
+        return c->fail(LMX_ENOMEM, "queue ring allocation (" + std::to_string(ring_entries) + " entries; lower qcap)");
+    if (c->summaries.ensure(std::max<int64_t>(T, 1) * sizeof(lmx_summary)) != cudaSuccess ||
+        c->trace_err.ensure(std::max<int64_t>(T, 1) * 8) != cudaSuccess ||
+        c->cell_i.ensure((size_t)c->n_cells * LMX_CELL_NI * 8) != cudaSuccess ||
+        c->cell_f.ensure((size_t)c->n_cells * LMX_CELL_NF * 8) != cudaSuccess)
+        return c->fail(LMX_ENOMEM, "summary allocation");
+    if (c->per_task) {
+        if (c->node_defer.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess ||
+            c->decision_idx.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess ||
+            c->completion.ensure(std::max<int64_t>(M, 1) * 8) != cudaSuccess ||
+            c->start_f1.ensure(std::max<int64_t>(M, 1) * 8) != cudaSuccess)
+            return c->fail(LMX_ENOMEM, "per-task output allocation");
+        k.node_defer = (uint32_t *)c->node_defer.p;
+        k.decision_idx = (int32_t *)c->decision_idx.p;
+        k.completion = (double *)c->completion.p;
+        k.start_f1 = (double *)c->start_f1.p;
+    }
+    k.summaries = (lmx_summary *)c->summaries.p;
+    k.trace_err = (int64_t *)c->trace_err.p;
+    k.work = (unsigned long long *)c->work.p;
+    k.first_bad = (unsigned long long *)c->first_bad.p;
+    k.ring_be = (double2 *)c->ring_be.p;
+    k.ring_w = (double *)c->ring_w.p;
+
+    lmx_status s = c->cuda(cudaMemsetAsync(c->work.p, 0, 8, c->stream), "reset");
+    if (s == LMX_OK) s = c->cuda(cudaMemsetAsync(c->first_bad.p, 0xFF, 8, c->stream), "reset");
+    if (s != LMX_OK) return s;
+    c->launches = 0;
+    cudaEventRecord(c->ev0, c->stream);
+    if (T > 0) {
+        int e = lmx::launch_event_loop(k, (int)grid, c->stream);
+        if (e != 0) return c->cuda((cudaError_t)e, "event loop launch");
+        c->launches++;
+    }
+    cudaEventRecord(c->ev1, c->stream);
+
+    lmx::CellParams cp{};
+    cp.n_traces = T;
+    cp.n_cells = c->n_cells;
+    cp.cell_of = c->cells_set ? (const int32_t *)c->cell_of.p : nullptr;
+    cp.summaries = (const lmx_summary *)c->summaries.p;
+    cp.cell_i = (int64_t *)c->cell_i.p;
+    cp.cell_f = (double *)c->cell_f.p;
+    int e = lmx::launch_cells(cp, c->stream);
+    if (e != 0) return c->cuda((cudaError_t)e, "cell reduction launch");
+    c->launches++;
+    cudaEventRecord(c->ev2, c->stream);
+
+    c->grid = (int32_t)grid;
+    c->block = block;
+    c->lanes = Tl;
+    c->smem = lmx::event_loop_smem_bytes(k);
+    c->ran = true;
+    c->synced = false;
+    return LMX_OK;
+}
+
+lmx_status lmx_sync(lmx_ctx *c)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran) return c->fail(LMX_ESTATE, "lmx_sync: nothing was run");
+    cudaSetDevice(c->device);
+    lmx_status s = c->cuda(cudaStreamSynchronize(c->stream), "lmx_run");
+    if (s != LMX_OK) return s;
+    c->synced = true;
+    unsigned long long bad = ~0ull;
+    s = c->cuda(cudaMemcpy(&bad, c->first_bad.p, 8, cudaMemcpyDeviceToHost), "status read");
+    if (s != LMX_OK) return s;
+    if (bad == ~0ull) return LMX_OK;
+    lmx_summary sm;
+    int64_t info = 0;
+    cudaMemcpy(&sm, (lmx_summary *)c->summaries.p + bad, sizeof sm, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&info, (int64_t *)c->trace_err.p + bad, 8, cudaMemcpyDeviceToHost);
+    const int64_t task = info >> 8;
+    const int code = (int)(info & 0xFF);
+    char buf[512];
+    if (sm.status == LMX_EINVAL)
+        snprintf(buf, sizeof buf, "trace %llu, task %lld: invalid %s", (unsigned long long)bad, (long long)task,
+                 field_name(code));
+    else if (sm.status == LMX_EQCAP)
+        snprintf(buf, sizeof buf, "trace %llu: a node's training queue exceeded params.qcap = %d", (unsigned long long)bad,
+                 c->par.qcap);
+    else
+        snprintf(buf, sizeof buf, "trace %llu: decision budget exhausted", (unsigned long long)bad);
+    c->err = buf;
+    return (lmx_status)sm.status;
+}
+
+static lmx_status copy_out(lmx_ctx *c, void *dst, const DevBuf &src, size_t bytes, lmx_mem mem, const char *what)
+{
+    if (!dst || bytes == 0) return LMX_OK;
+    return c->cuda(cudaMemcpy(dst, src.p, bytes, mem == LMX_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost),
+                   what);
+}
+
+lmx_status lmx_get_assignments(lmx_ctx *c, uint32_t *node_defer, int32_t *decision_idx, lmx_mem mem)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran || !c->synced) return c->fail(LMX_ESTATE, "lmx_get_assignments: run and sync first");
+    if (!c->per_task) return c->fail(LMX_ESTATE, "per-task outputs are off (lmx_set_outputs)");
+    cudaSetDevice(c->device);
+    lmx_status s = copy_out(c, node_defer, c->node_defer, c->n_tasks * 4, mem, "node_defer copy");
+    if (s == LMX_OK) s = copy_out(c, decision_idx, c->decision_idx, c->n_tasks * 4, mem, "decision_idx copy");
+    return s;
+}
+
+lmx_status lmx_get_times(lmx_ctx *c, double *completion, double *start_f1, lmx_mem mem)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran || !c->synced) return c->fail(LMX_ESTATE, "lmx_get_times: run and sync first");
+    if (!c->per_task) return c->fail(LMX_ESTATE, "per-task outputs are off (lmx_set_outputs)");
+    cudaSetDevice(c->device);
+    lmx_status s = copy_out(c, completion, c->completion, c->n_tasks * 8, mem, "completion copy");
+    if (s == LMX_OK) s = copy_out(c, start_f1, c->start_f1, c->n_tasks * 8, mem, "start_f1 copy");
+    return s;
+}
+
+lmx_status lmx_get_summaries(lmx_ctx *c, lmx_summary *per_trace)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran || !c->synced) return c->fail(LMX_ESTATE, "lmx_get_summaries: run and sync first");
+    cudaSetDevice(c->device);
+    return copy_out(c, per_trace, c->summaries, c->n_traces * sizeof(lmx_summary), LMX_HOST, "summary copy");
+}
+
+lmx_status lmx_get_cells(lmx_ctx *c, lmx_cell_summary *cells)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran) return c->fail(LMX_ESTATE, "lmx_get_cells: run first");
+    if (!cells) return c->fail(LMX_EINVAL, "lmx_get_cells: NULL output");
+    cudaSetDevice(c->device);
+    std::vector<int64_t> hi((size_t)c->n_cells * LMX_CELL_NI);
+    std::vector<double> hf((size_t)c->n_cells * LMX_CELL_NF);
+    lmx_status s = c->cuda(cudaMemcpyAsync(hi.data(), c->cell_i.p, hi.size() * 8, cudaMemcpyDeviceToHost, c->stream),
+                           "cell copy");
+    if (s == LMX_OK)
+        s = c->cuda(cudaMemcpyAsync(hf.data(), c->cell_f.p, hf.size() * 8, cudaMemcpyDeviceToHost, c->stream),
+                    "cell copy");
+    if (s == LMX_OK) s = c->cuda(cudaStreamSynchronize(c->stream), "cell copy");
+    if (s != LMX_OK) return s;
+    for (int32_t q = 0; q < c->n_cells; ++q) {
+        int64_t *I = &hi[(size_t)q * LMX_CELL_NI];
+        double *F = &hf[(size_t)q * LMX_CELL_NF];
+        lmx_cell_summary &o = cells[q];
+        o.n_traces = I[0]; o.n_failed = I[1]; o.n_tasks = I[2]; o.n_inf = I[3]; o.n_train = I[4];
+        o.n_slo_met = I[5]; o.n_deferrals = I[6]; o.sum_active_nodes = I[7]; o.sum_version = I[8];
+        o.sum_makespan = F[0]; o.sum_throughput = F[1]; o.sum_ttft = F[2]; o.sum_mean_ttft = F[3];
+        o.sum_slo_attainment = F[4]; o.sum_mean_util = F[5]; o.sum_mean_len_std = F[6];
+    }
+    return LMX_OK;
+}
+
+lmx_status lmx_allreduce_cells(lmx_ctx *c, void *comm)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran) return c->fail(LMX_ESTATE, "lmx_allreduce_cells: run first");
+    if (!comm) return c->fail(LMX_EINVAL, "lmx_allreduce_cells: NULL communicator");
+    if (!g_nccl.load()) return c->fail(LMX_ENCCL, "libnccl.so.2 not found");
+    cudaSetDevice(c->device);
+    int r = g_nccl.group_start();
+    if (r == 0) r = g_nccl.all_reduce(c->cell_i.p, c->cell_i.p, (size_t)c->n_cells * LMX_CELL_NI, kNcclInt64, kNcclSum,
+                                      comm, c->stream);
+    if (r == 0) r = g_nccl.all_reduce(c->cell_f.p, c->cell_f.p, (size_t)c->n_cells * LMX_CELL_NF, kNcclFloat64,
+                                      kNcclSum, comm, c->stream);
+    int r2 = g_nccl.group_end();
+    if (r != 0 || r2 != 0) return c->fail(LMX_ENCCL, "ncclAllReduce failed (" + std::to_string(r ? r : r2) + ")");
+    return LMX_OK;
+}
+
+lmx_status lmx_nccl_unique_id(void *id128)
+{
+    if (!id128) return LMX_EINVAL;
+    if (!g_nccl.load()) return LMX_ENCCL;
+    return g_nccl.get_unique_id(id128) == 0 ? LMX_OK : LMX_ENCCL;
+}
+
+lmx_status lmx_nccl_comm_init(void **comm, int nranks, const void *id128, int rank, int device)
+{
+    if (!comm || !id128 || nranks < 1 || rank < 0 || rank >= nranks) return LMX_EINVAL;
+    if (!g_nccl.load()) return LMX_ENCCL;
+    if (cudaSetDevice(device) != cudaSuccess) return LMX_ECUDA;
+    NcclId128 id;
+    std::memcpy(id.internal, id128, 128);
+    return g_nccl.comm_init_rank(comm, nranks, id, rank) == 0 ? LMX_OK : LMX_ENCCL;
+}
+
+lmx_status lmx_nccl_comm_destroy(void *comm)
+{
+    if (!comm) return LMX_OK;
+    if (!g_nccl.load()) return LMX_ENCCL;
+    return g_nccl.comm_destroy(comm) == 0 ? LMX_OK : LMX_ENCCL;
+}
+
+lmx_status lmx_get_timing(lmx_ctx *c, float *kernel_ms, float *run_ms, int32_t *launches)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran || !c->synced) return c->fail(LMX_ESTATE, "lmx_get_timing: run and sync first");
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, c->ev0, c->ev1);
+    cudaEventElapsedTime(&b, c->ev0, c->ev2);
+    if (kernel_ms) *kernel_ms = a;
+    if (run_ms) *run_ms = b;
+    if (launches) *launches = c->launches;
+    return LMX_OK;
+}
+
+lmx_status lmx_get_geometry(lmx_ctx *c, int32_t *grid, int32_t *block, int32_t *lanes, int32_t *smem)
+{
+    if (!c) return LMX_EINVAL;
+    if (grid) *grid = c->grid;
+    if (block) *block = c->block;
+    if (lanes) *lanes = c->lanes;
+    if (smem) *smem = c->smem;
+    return LMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// lemix_internal.h -- host<->device contract between lemix_api.cpp and
+// lemix_kernels.cu (not part of the public ABI; see include/lemix.h).
+#pragma once
+#include <cstdint>
+
+#include "lemix.h"
+
+namespace lmx {
+
+// Everything the persistent event-loop kernel needs, passed by value.
+struct KParams {
+    // geometry of the candidate sweep: a "tile" of T lanes owns one trace,
+    // lane l handles nodes l, l+T, l+2T, ... (npl slots)
+    int32_t N, S, T, log2T, npl;
+    int32_t policy, deprioritize, slo_mode;
+    int32_t qcap;        // logical capacity of Q_train^n
+    int32_t kmask;       // ring allocation K - 1 (K = next power of two >= qcap)
+    int32_t n_tr_sep;    // Separate: N_train when both kinds are present (host-computed)
+    int32_t s_pow2;      // S is a power of two -> II/S == II * (1/S) exactly
+    double inv_S;
+    double lambda1, lambda2, tau, slo_mult, slo_const, sigma_floor, lc0;
+
+    int64_t n_traces;
+    const int64_t *offsets;    // device [n_traces+1]
+    const int32_t *n_inf;      // device [n_traces]
+    const double *arrival;     // device [n_tasks]
+    const uint32_t *lbk;       // device [n_tasks]
+    const int32_t *fixed;      // device [n_tasks] or nullptr
+    const double *eta;         // device [2*N*S]: eta_f then eta_b, node-major
+
+    uint32_t *node_defer;      // outputs, nullptr = summary-only
+    int32_t *decision_idx;
+    double *completion;
+    double *start_f1;
+
+    lmx_summary *summaries;    // device [n_traces]
+    int64_t *trace_err;        // device [n_traces]: (task << 8) | field code, -1 none
+    unsigned long long *work;  // device [1]: next trace to claim
+    unsigned long long *first_bad;  // device [1]: min failing trace index
+
+    double2 *ring_be;          // [tile_slots][Npad][K][S] (start_b, end_b)
+    double *ring_w;            // [tile_slots][Npad][K]    C*l^2 of the entry
+    int32_t npad;              // npl * T
+};
+
+// field codes for trace_err (reported by lmx_last_error)
+enum : int32_t {
+    kErrNone = 0, kErrLen = 1, kErrBatch = 2, kErrKind = 3, kErrBits = 4, kErrArrival = 5,
+    kErrOrder = 6, kErrFixed = 7, kErrSeparateN1 = 8
+};
+
+struct CellParams {
+    int64_t n_traces;
+    int32_t n_cells;
+    const int32_t *cell_of;    // device [n_traces] or nullptr (all in cell 0)
+    const lmx_summary *summaries;
+    int64_t *cell_i;           // [n_cells][LMX_CELL_NI]
+    double *cell_f;            // [n_cells][LMX_CELL_NF]
+};
+
+// launchers (lemix_kernels.cu)
+int max_stages_bucket(int S);                         // template bucket for S
+int npl_bucket(int npl);                              // template bucket for nodes/lane
+int event_loop_smem_bytes(const KParams &p);
+int event_loop_block_threads();
+// blocks per SM the event loop can keep resident with this geometry
+int event_loop_occupancy(const KParams &p, int *err);
+int launch_event_loop(const KParams &p, int grid, void *stream);
+int launch_cells(const CellParams &c, void *stream);
+
+}  // namespace lmx

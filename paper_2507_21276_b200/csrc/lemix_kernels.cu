@@ -1,0 +1,622 @@
+// lemix_kernels.cu -- sm_100a kernels of the LeMix placement step.
+//
+// K1 profile staging : the fp64 SoA profile table (eta_f, eta_b) is copied
+//                      into shared memory once per CTA with a TMA bulk copy
+//                      (cp.async.bulk + mbarrier).
+// K2-K4 event loop   : one persistent kernel.  A "tile" of T lanes of a warp
+//                      owns one trace at a time; lane l plans nodes l, l+T, ...
+//                      (Algorithm 1) and scores them (Eq. 1-3,
+//                      PAPER.md:546-565); a tile shuffle takes the arg-best with
+//                      the lowest-index tie-break; the owning
+//                      lane commits.  Eq. 4 is a tile min.
+//                      Tiles claim traces from a global counter until none are
+//                      left, so long and short traces balance across SMs.
+// K5 cell reduction  : per-cell sums of the per-trace summaries in a fixed
+//                      order (deterministic), ready for one NCCL all-reduce.
+//
+// Compiled with --fmad=false: see lemix_device.cuh for the fp64 discipline.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+
+#include "lemix_device.cuh"
+#include "lemix_internal.h"
+
+namespace lmx {
+
+namespace {
+
+constexpr int kBlock = 128;                 // 4 warps per CTA
+constexpr double kInf = __builtin_huge_val();
+constexpr double kSqrt2Pi = 0x1.40d931ff62705p+1;
+
+__device__ __forceinline__ int task_len(uint32_t v) { return (int)(v & 0xFFFu); }
+__device__ __forceinline__ int task_batch(uint32_t v) { return (int)((v >> 12) & 0xFFu); }
+// C * l^2, exact in int64 and as a double (< 2^31)
+__device__ __forceinline__ double task_w(uint32_t v)
+{
+    const long long l = task_len(v), c = task_batch(v);
+    return (double)(c * l * l);
+}
+
+template <int SMAX, int NPL>
+__global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t s_bar;
+
+    const int N = p.N, S = p.S, NS = p.N * p.S;
+    double *s_eta = reinterpret_cast<double *>(smem_raw);
+
+    // ---- K1: stage eta_f | eta_b (16*N*S bytes) into shared memory via TMA ----
+    if (threadIdx.x == 0) {
+        dev::mbar_init(&s_bar, 1);
+        dev::mbar_arrive_expect_tx(&s_bar, 16u * (uint32_t)NS);
+        dev::bulk_copy_g2s(s_eta, p.eta, 16u * (uint32_t)NS, &s_bar);
+    }
+    __syncthreads();
+    dev::mbar_wait(&s_bar, 0);
+    const double *s_ef = s_eta;
+    const double *s_eb = s_eta + NS;
+
+    // ---- tile geometry ----
+    const int lane = threadIdx.x & 31;
+    const int T = p.T, log2T = p.log2T;
+    const int tl = lane & (T - 1);
+    const int tbase = lane & ~(T - 1);
+    const unsigned tmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << tbase);
+    const long long gtile = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> log2T;
+    const long long K = (long long)p.kmask + 1;
+
+    long long rbase[NPL];   // first ring entry of this lane's nodes
+#pragma unroll
+    for (int jj = 0; jj < NPL; ++jj) rbase[jj] = (gtile * p.npad + (tl + jj * T)) * K;
+
+    // ---- per-trace (tile-replicated) state ----
+    bool active = false, finished = false;
+    long long t = 0, o = 0;
+    int nI = 0, nT = 0, i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0;
+    int cur_defer = 0, status = LMX_OK, err_task = 0, err_code = kErrNone;
+    double r = kInf, t_first = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
+    long long n_slo = 0, sum_ver = 0, n_def = 0;
+    double a_inf = 0.0, a_inf2 = 0.0, a_tr = 0.0, a_tr2 = 0.0;   // 2-deep input prefetch
+    uint32_t v_inf = 0, v_inf2 = 0, v_tr = 0, v_tr2 = 0;
+
+    // ---- per-node state of this lane's slots (registers) ----
+    double P[NPL][SMAX], LB[NPL][SMAX], busy[NPL][SMAX];
+    double aprev[NPL], mu[NPL], kk[NPL], cc[NPL];
+    int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL], ntr[NPL];
+    long long sl[NPL], sl2[NPL];
+
+    while (!__all_sync(0xffffffffu, finished)) {
+        if (finished) continue;
+        if (!active) {
+            // ---- claim the next trace ----
+            unsigned long long tt = 0;
+            if (tl == 0) tt = atomicAdd(p.work, 1ull);
+            tt = __shfl_sync(tmask, tt, tbase);
+            if (tt >= (unsigned long long)p.n_traces) {
+                finished = true;
+                continue;
+            }
+            t = (long long)tt;
+            o = p.offsets[t];
+            const int len = (int)(p.offsets[t + 1] - o);
+            nI = p.n_inf[t];
+            nT = len - nI;
+            i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
+            status = LMX_OK;
+            err_task = 0;
+            err_code = kErrNone;
+            n_slo = sum_ver = n_def = 0;
+            sum_ttft = 0.0;
+            t_last = -kInf;
+            a_last_inf = -kInf;
+            if (nI > 0) { a_inf = __ldg(p.arrival + o); v_inf = __ldg(p.lbk + o); }
+            if (nI > 1) { a_inf2 = __ldg(p.arrival + o + 1); v_inf2 = __ldg(p.lbk + o + 1); }
+            if (nT > 0) { a_tr = __ldg(p.arrival + o + nI); v_tr = __ldg(p.lbk + o + nI); }
+            if (nT > 1) { a_tr2 = __ldg(p.arrival + o + nI + 1); v_tr2 = __ldg(p.lbk + o + nI + 1); }
+            r = (nT > 0) ? a_tr : kInf;
+            t_first = kInf;
+            if (nI > 0) t_first = dev::dmin(t_first, a_inf);
+            if (nT > 0) t_first = dev::dmin(t_first, a_tr);
+#pragma unroll
+            for (int jj = 0; jj < NPL; ++jj) {
+                hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = ntr[jj] = 0;
+                sl[jj] = sl2[jj] = 0;
+                aprev[jj] = mu[jj] = kk[jj] = cc[jj] = 0.0;
+#pragma unroll
+                for (int s = 0; s < SMAX; ++s) { P[jj][s] = 0.0; LB[jj][s] = -kInf; busy[jj][s] = 0.0; }
+            }
+            if (p.policy == LMX_SEPARATE && N == 1 && nI > 0 && nT > 0) {
+                status = LMX_EINVAL;
+                err_code = kErrSeparateN1;
+            }
+            active = true;
+        }
+
+        bool done_trace = (status != LMX_OK) || (i >= nI && j >= nT);
+        if (!done_trace && ++iters > 2 * (nI + nT) + 2) {
+            status = LMX_EBUDGET;
+            done_trace = true;
+        }
+
+        if (done_trace) {
+            // ---- per-trace metrics, node folds in node order ----
+            lmx_summary sm;
+            sm.n_tasks = nI + nT;
+            sm.n_inf = nI;
+            sm.n_train = nT;
+            sm.status = status;
+            sm.n_slo_met = sm.n_deferrals = sm.active_nodes = sm.sum_version = 0;
+            sm.makespan = sm.throughput = sm.sum_ttft = sm.mean_ttft = sm.slo_attainment = 0.0;
+            sm.mean_util = sm.mean_len_std = 0.0;
+            if (status == LMX_OK) {
+                const int ntask = nI + nT;
+                sm.n_slo_met = n_slo;
+                sm.n_deferrals = n_def;
+                sm.sum_version = sum_ver;
+                sm.sum_ttft = sum_ttft;
+                sm.makespan = (ntask > 0) ? t_last - t_first : 0.0;
+                sm.throughput = (sm.makespan > 0.0) ? (double)ntask / sm.makespan : 0.0;
+                sm.mean_ttft = (nI > 0) ? sum_ttft / (double)nI : 0.0;
+                sm.slo_attainment = (nI > 0) ? (double)n_slo / (double)nI : 1.0;
+                double U = 0.0, stds = 0.0;
+                long long act = 0;
+                for (int n = 0; n < N; ++n) {
+                    const int src = tbase + (n & (T - 1));
+                    const int jn = n >> log2T;
+                    long long c = 0, v2 = 0;
+#pragma unroll
+                    for (int jj = 0; jj < NPL; ++jj)
+                        if (jj == jn) { c = cnt[jj]; v2 = (long long)cnt[jj] * sl2[jj] - sl[jj] * sl[jj]; }
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) {
+                        if (s < S) {
+                            double b = 0.0;
+#pragma unroll
+                            for (int jj = 0; jj < NPL; ++jj)
+                                if (jj == jn) b = busy[jj][s];
+                            U = U + dev::shfl_d(tmask, b, src);
+                        }
+                    }
+                    double sd = (c > 0) ? sqrt((double)v2) / (double)c : 0.0;
+                    sd = dev::shfl_d(tmask, sd, src);
+                    c = __shfl_sync(tmask, c, src);
+                    if (c > 0) {
+                        act++;
+                        stds = stds + sd;
+                    }
+                }
+                sm.active_nodes = act;
+                sm.mean_util = (sm.makespan > 0.0) ? U / ((double)(N * S) * sm.makespan) : 0.0;
+                sm.mean_len_std = (act > 0) ? stds / (double)act : 0.0;
+            }
+            if (tl == 0) {
+                p.summaries[t] = sm;
+                if (status != LMX_OK) {
+                    p.trace_err[t] = ((long long)err_task << 8) | err_code;
+                    atomicMin(p.first_bad, (unsigned long long)t);
+                }
+            }
+            active = false;
+            continue;
+        }
+
+        // ---- a1: event selection (ties -> inference) ----
+        const double t_inf = (i < nI) ? a_inf : kInf;
+        const bool is_train = !(t_inf <= r);
+        double now;
+        uint32_t v;
+        if (!is_train) {
+            now = t_inf;
+            v = v_inf;
+        } else {
+            now = r;
+            v = v_tr;
+            // ---- a2: Eq. 4 queue-level deprioritisation against the next
+            // enqueued inference task (R-14/R-15) ----
+            if (p.policy == LMX_LEMIX && p.deprioritize && i < nI) {
+                const double wn = task_w(v_inf);
+                double m = kInf;
+#pragma unroll
+                for (int jj = 0; jj < NPL; ++jj) {
+                    const int n = tl + jj * T;
+                    if (n < N) {
+                        const double latest = hasp[jj] ? P[jj][S - 1] : -kInf;
+                        m = dev::dmin(m, latest + s_ef[n * S + S - 1] * wn);
+                    }
+                }
+                for (int off = T >> 1; off > 0; off >>= 1) m = dev::dmin(m, dev::shfl_xor_d(tmask, m, off));
+                double tauR;
+                if (p.slo_mode == 1) {
+                    tauR = p.slo_const;
+                } else {
+                    double acc = 0.0;
+                    for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * wn;
+                    tauR = p.slo_mult * acc;
+                }
+                if ((m - t_inf) > tauR) {
+                    r = t_inf;          // move behind the next inference task
+                    cur_defer++;
+                    n_def++;
+                    continue;
+                }
+            }
+        }
+        const int task = is_train ? nI + j : i;
+
+        // ---- input validation of the task being placed ----
+        {
+            const double arr = is_train ? a_tr : a_inf;
+            int code = kErrNone;
+            if (v >> 21) code = kErrBits;
+            else if (task_len(v) < 1 || task_len(v) > 2048) code = kErrLen;
+            else if (task_batch(v) < 1) code = kErrBatch;
+            else if ((int)((v >> 20) & 1u) != (int)is_train) code = kErrKind;
+            else if (!(arr >= 0.0 && arr < kInf)) code = kErrArrival;
+            else if (!is_train && arr < a_last_inf) code = kErrOrder;
+            int fx = 0;
+            if (p.policy == LMX_FIXED) {
+                fx = __ldg(p.fixed + o + task);
+                if (code == kErrNone && (fx < 0 || fx >= N)) code = kErrFixed;
+            }
+            if (code != kErrNone) {
+                status = LMX_EINVAL;
+                err_task = task;
+                err_code = code;
+                continue;
+            }
+        }
+
+        const double a = now;                    // dispatch time (R-2)
+        const double w = task_w(v);
+        const int l = task_len(v);
+
+        // ---- a9: baseline selectors ----
+        int chosen = -1;
+        if (p.policy == LMX_RR) {
+            chosen = rr % N;
+            rr++;
+        } else if (p.policy == LMX_SEPARATE) {
+            if (!(nI > 0 && nT > 0)) {
+                chosen = is_train ? (sep_t++ % N) : (sep_i++ % N);
+            } else if (is_train) {
+                chosen = (N - p.n_tr_sep) + (sep_t++ % p.n_tr_sep);
+            } else {
+                chosen = sep_i++ % (N - p.n_tr_sep);
+            }
+        } else if (p.policy == LMX_FIXED) {
+            chosen = __ldg(p.fixed + o + task);
+        }
+
+        // ---- a3-a7: Algorithm 1 + Eq. 1-3 for every candidate this lane owns ----
+        double en_s[NPL][SMAX];
+        double st0_s[NPL];
+        double f_best = 0.0;
+        int n_best = INT_MAX;
+#pragma unroll
+        for (int jj = 0; jj < NPL; ++jj) {
+            const int n = tl + jj * T;
+            st0_s[jj] = 0.0;
+#pragma unroll
+            for (int s = 0; s < SMAX; ++s) en_s[jj][s] = 0.0;
+            if (n < N && (p.policy == LMX_LEMIX || n == chosen)) {
+                const double *ef = s_ef + n * S;
+                const double *eb = s_eb + n * S;
+                // line 3: task_prev; a never-used node has a virtual predecessor (R-1)
+                double Pv[SMAX];
+                if (hasp[jj]) {
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) Pv[s] = P[jj][s];
+                } else {
+                    double vv = a;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s)
+                        if (s < S) { Pv[s] = vv; vv = vv + ef[s] * w; }
+                }
+                double II = 0.0, e = a;
+                int cur = 0, gc = 0;
+                const int qhead = qh[jj], qlen = qn[jj];
+#pragma unroll
+                for (int s = 0; s < SMAX; ++s) {                    // line 4
+                    if (s < S) {
+                        const double dF = ef[s] * w;
+                        double st = dev::dmax(e, Pv[s]);            // line 5
+                        double en = st + dF;                        // line 6
+                        double off = 0.0;                           // line 7
+                        while (cur < qlen) {                        // lines 8-9 (Q_temp = cursor)
+                            const long long idx = rbase[jj] + ((qhead + cur) & p.kmask);
+                            const double2 q = p.ring_be[idx * S + s];   // (start_b^s, end_b^s)
+                            if (en <= q.x) break;                   // lines 10-12: stays at the front
+                            st = dev::dmax(st, q.y);                // line 13
+                            en = st + dF;                           // line 14
+                            if (Pv[s] <= q.x) off = off + eb[s] * p.ring_w[idx];   // lines 15-16
+                            if (s == 0 && q.y <= now) gc = cur + 1; // lines 17-18 CheckExecuted
+                            cur++;
+                        }
+                        II = II + ((st - Pv[s]) - off);             // line 19
+                        en_s[jj][s] = en;
+                        if (s == 0) st0_s[jj] = st;
+                        e = en;
+                    }
+                }
+                // lines 17-18: executed entries leave Q_train^n (a head advance:
+                // end_b^1 is non-decreasing along the queue)
+                qh[jj] = qhead + gc;
+                qn[jj] = qlen - gc;
+                if (p.policy == LMX_LEMIX) {
+                    const double R = e - a;                                       // line 20
+                    const double a_last = hasp[jj] ? aprev[jj] : a;               // R-9
+                    const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
+                    const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
+                    double LC;                                                    // Eq. 2
+                    if (cnt[jj] < 2) {
+                        LC = p.lc0;
+                    } else {
+                        const double d = (double)l - mu[jj];
+                        LC = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
+                    }
+                    const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
+                    if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
+                }
+            }
+        }
+
+        // ---- a8: arg-best over the tile: highest f, then lowest node index ----
+        int best;
+        if (p.policy == LMX_LEMIX) {
+            for (int off = T >> 1; off > 0; off >>= 1) {
+                const double f2 = dev::shfl_xor_d(tmask, f_best, off);
+                const int n2 = __shfl_xor_sync(tmask, n_best, off);
+                if (n2 != INT_MAX &&
+                    (n_best == INT_MAX || f2 > f_best || (f2 == f_best && n2 < n_best))) {
+                    f_best = f2;
+                    n_best = n2;
+                }
+            }
+            best = n_best;
+        } else {
+            best = chosen;
+        }
+
+        // ---- a10: commit on the owning lane ----
+        const int owner = tbase + (best & (T - 1));
+        const int jb = best >> log2T;
+        double c_done = 0.0, c_en0 = 0.0, c_enS = 0.0, c_st0 = 0.0;
+        int c_ver = 0, c_status = LMX_OK;
+        if (lane == owner) {
+#pragma unroll
+            for (int jj = 0; jj < NPL; ++jj) {
+                if (jj == jb) {
+                    const double *ef = s_ef + best * S;
+                    const double *eb = s_eb + best * S;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s)
+                        if (s < S) {
+                            P[jj][s] = en_s[jj][s];
+                            busy[jj][s] = busy[jj][s] + ef[s] * w;
+                        }
+                    hasp[jj] = 1;
+                    aprev[jj] = a;
+                    c_en0 = en_s[jj][0];
+                    c_enS = en_s[jj][S - 1];
+                    c_st0 = st0_s[jj];
+                    if (is_train) {
+                        if (qn[jj] >= p.qcap) {
+                            c_status = LMX_EQCAP;
+                        } else {
+                            // backward planning, stages S..1
+                            const long long idx = rbase[jj] + ((qh[jj] + qn[jj]) & p.kmask);
+                            double x = c_enS;
+#pragma unroll
+                            for (int s = SMAX - 1; s >= 0; --s) {
+                                if (s < S) {
+                                    const double sb = dev::dmax(x, LB[jj][s]);
+                                    const double ebv = sb + eb[s] * w;
+                                    LB[jj][s] = ebv;
+                                    p.ring_be[idx * S + s] = make_double2(sb, ebv);
+                                    x = ebv;
+                                }
+                            }
+                            p.ring_w[idx] = w;
+                            qn[jj]++;
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) busy[jj][s] = busy[jj][s] + eb[s] * w;
+                            ntr[jj]++;
+                            c_done = x;
+                        }
+                    } else {
+                        c_done = c_enS;
+                        // version-at-inference: completed training tasks on this
+                        // node at the forward start.  end_b^1 is non-decreasing
+                        // along the queue, so the completed ones form a prefix.
+                        int k = 0;
+                        while (k < qn[jj] &&
+                               p.ring_be[(rbase[jj] + ((qh[jj] + k) & p.kmask)) * S].y <= c_st0)
+                            k++;
+                        c_ver = ntr[jj] - (qn[jj] - k);
+                    }
+                    cnt[jj]++;
+                    sl[jj] += l;
+                    sl2[jj] += (long long)l * l;
+                    if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (population mean / sigma)
+                        const long long c = cnt[jj];
+                        mu[jj] = (double)sl[jj] / (double)c;
+                        const long long var = c * sl2[jj] - sl[jj] * sl[jj];
+                        const double sigma = dev::dmax(sqrt((double)var) / (double)c, p.sigma_floor);
+                        kk[jj] = 0.5 / (sigma * sigma);
+                        cc[jj] = 1.0 / (sigma * kSqrt2Pi);
+                    }
+                }
+            }
+        }
+        c_done = dev::shfl_d(tmask, c_done, owner);
+        c_en0 = dev::shfl_d(tmask, c_en0, owner);
+        c_enS = dev::shfl_d(tmask, c_enS, owner);
+        c_st0 = dev::shfl_d(tmask, c_st0, owner);
+        c_ver = __shfl_sync(tmask, c_ver, owner);
+        c_status = __shfl_sync(tmask, c_status, owner);
+        if (c_status != LMX_OK) {
+            status = c_status;
+            continue;
+        }
+
+        // ---- a11: outputs + per-trace folds ----
+        if (tl == 0 && p.node_defer) {
+            const unsigned dsat = is_train ? (unsigned)min(cur_defer, 0xFFFF) : 0u;
+            p.node_defer[o + task] = (uint32_t)best | (dsat << 16);
+            p.decision_idx[o + task] = step;
+            p.completion[o + task] = c_done;
+            p.start_f1[o + task] = c_st0;
+        }
+        t_last = dev::dmax(t_last, c_done);
+        step++;
+        if (is_train) {
+            j++;
+            cur_defer = 0;
+            a_tr = a_tr2;
+            v_tr = v_tr2;
+            if (j + 1 < nT) {
+                a_tr2 = __ldg(p.arrival + o + nI + j + 1);
+                v_tr2 = __ldg(p.lbk + o + nI + j + 1);
+            }
+            // next release: max(a_min, this task's S1 forward end)
+            r = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
+        } else {
+            const double ttft = c_enS - a;         // R from arrival
+            sum_ttft = sum_ttft + ttft;
+            double tauR;
+            if (p.slo_mode == 1) {
+                tauR = p.slo_const;
+            } else {
+                double acc = 0.0;
+                for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * w;
+                tauR = p.slo_mult * acc;
+            }
+            if (ttft <= tauR) n_slo++;              // SLO: TTFT <= 5x forward latency
+            sum_ver += c_ver;
+            a_last_inf = a;
+            i++;
+            a_inf = a_inf2;
+            v_inf = v_inf2;
+            if (i + 1 < nI) {
+                a_inf2 = __ldg(p.arrival + o + i + 1);
+                v_inf2 = __ldg(p.lbk + o + i + 1);
+            }
+        }
+    }
+}
+
+// ---- K5: per-cell sums of the per-trace summaries, fixed order ----
+constexpr int kCellBlock = 256;
+
+__global__ void __launch_bounds__(kCellBlock) cells_kernel(const CellParams c)
+{
+    __shared__ long long si[kCellBlock][LMX_CELL_NI];
+    __shared__ double sf[kCellBlock][LMX_CELL_NF];
+    const int cell = blockIdx.x;
+    long long ai[LMX_CELL_NI];
+    double af[LMX_CELL_NF];
+#pragma unroll
+    for (int k = 0; k < LMX_CELL_NI; ++k) ai[k] = 0;
+#pragma unroll
+    for (int k = 0; k < LMX_CELL_NF; ++k) af[k] = 0.0;
+    for (long long t = threadIdx.x; t < c.n_traces; t += kCellBlock) {
+        const int ct = c.cell_of ? c.cell_of[t] : 0;
+        if (ct != cell) continue;
+        const lmx_summary s = c.summaries[t];
+        ai[0] += 1;
+        if (s.status != LMX_OK) { ai[1] += 1; continue; }
+        ai[2] += s.n_tasks; ai[3] += s.n_inf; ai[4] += s.n_train; ai[5] += s.n_slo_met;
+        ai[6] += s.n_deferrals; ai[7] += s.active_nodes; ai[8] += s.sum_version;
+        af[0] = af[0] + s.makespan; af[1] = af[1] + s.throughput; af[2] = af[2] + s.sum_ttft;
+        af[3] = af[3] + s.mean_ttft; af[4] = af[4] + s.slo_attainment; af[5] = af[5] + s.mean_util;
+        af[6] = af[6] + s.mean_len_std;
+    }
+#pragma unroll
+    for (int k = 0; k < LMX_CELL_NI; ++k) si[threadIdx.x][k] = ai[k];
+#pragma unroll
+    for (int k = 0; k < LMX_CELL_NF; ++k) sf[threadIdx.x][k] = af[k];
+    __syncthreads();
+    for (int h = kCellBlock / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+#pragma unroll
+            for (int k = 0; k < LMX_CELL_NI; ++k) si[threadIdx.x][k] += si[threadIdx.x + h][k];
+#pragma unroll
+            for (int k = 0; k < LMX_CELL_NF; ++k) sf[threadIdx.x][k] = sf[threadIdx.x][k] + sf[threadIdx.x + h][k];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < LMX_CELL_NI; ++k) c.cell_i[cell * LMX_CELL_NI + k] = si[0][k];
+#pragma unroll
+        for (int k = 0; k < LMX_CELL_NF; ++k) c.cell_f[cell * LMX_CELL_NF + k] = sf[0][k];
+    }
+}
+
+typedef void (*kernel_fn)(const KParams);
+
+template <int SMAX>
+kernel_fn pick_npl(int npl)
+{
+    switch (npl) {
+    case 1: return event_loop_kernel<SMAX, 1>;
+    case 2: return event_loop_kernel<SMAX, 2>;
+    default: return event_loop_kernel<SMAX, 4>;
+    }
+}
+
+kernel_fn pick(const KParams &p)
+{
+    switch (max_stages_bucket(p.S)) {
+    case 1: return pick_npl<1>(npl_bucket(p.npl));
+    case 2: return pick_npl<2>(npl_bucket(p.npl));
+    case 4: return pick_npl<4>(npl_bucket(p.npl));
+    case 8: return pick_npl<8>(npl_bucket(p.npl));
+    default: return pick_npl<16>(npl_bucket(p.npl));
+    }
+}
+
+}  // namespace
+
+int max_stages_bucket(int S)
+{
+    return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16;
+}
+
+int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
+
+int event_loop_smem_bytes(const KParams &p) { return 16 * p.N * p.S; }
+
+int event_loop_block_threads() { return kBlock; }
+
+int event_loop_occupancy(const KParams &p, int *err)
+{
+    kernel_fn f = pick(p);
+    const int smem = event_loop_smem_bytes(p);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int blocks = 0;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, smem);
+    *err = (int)e;
+    return blocks;
+}
+
+int launch_event_loop(const KParams &p, int grid, void *stream)
+{
+    kernel_fn f = pick(p);
+    const int smem = event_loop_smem_bytes(p);
+    f<<<grid, kBlock, smem, (cudaStream_t)stream>>>(p);
+    return (int)cudaGetLastError();
+}
+
+int launch_cells(const CellParams &c, void *stream)
+{
+    cells_kernel<<<c.n_cells, kCellBlock, 0, (cudaStream_t)stream>>>(c);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace lmx

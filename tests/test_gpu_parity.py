@@ -1,0 +1,115 @@
+"""GPU (CUDA path through the C ABI) vs CPU oracle, element by element.
+
+Integers and indices bit-exact; fp64 per-task times and summaries bit-exact by
+construction and in any case within 1e-12 relative (north_star)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import workload
+from parity_util import check, run_both, compare_summaries, compare_tasks
+
+pytestmark = pytest.mark.gpu
+
+lemix = pytest.importorskip("paper_2507_21276_b200.lemix")
+
+
+def P(**kw):
+    return lemix.Params(**kw)
+
+
+POLICIES = [lemix.LMX_LEMIX, lemix.LMX_RR, lemix.LMX_SEPARATE]
+
+
+# ---------------------------------------------------------------- tiny config
+@pytest.mark.parametrize("N,S", [(4, 2), (2, 4)])
+@pytest.mark.parametrize("policy", POLICIES)
+def test_tiny(N, S, policy):
+    tr = workload.generate(workload.tiny_spec(), 1, seed_base=1)
+    check(N, S, tr, P(policy=policy))
+
+
+def test_tiny_fixed():
+    tr = workload.generate(workload.tiny_spec(), 4, seed_base=11)
+    rng = np.random.default_rng(5)
+    fixed = rng.integers(0, 4, tr.n_tasks).astype(np.int32)
+    check(4, 2, tr, P(policy=lemix.LMX_FIXED), fixed=fixed)
+
+
+# ---------------------------------------------------------------- paper scale
+def test_paper_scale():
+    tr = workload.generate(workload.paper_spec(), 3, seed_base=1)
+    check(4, 2, tr, P())
+
+
+# ---------------------------------------------------------------- sweep
+@pytest.mark.parametrize("policy", POLICIES)
+def test_sweep_cells(policy):
+    parts = [workload.generate(workload.sweep_spec(rate), 16, seed_base=1000 + 16 * k)
+             for k, rate in enumerate(workload.SWEEP_RATES)]
+    tr = workload.concat(parts)
+    cells = np.repeat(np.arange(16, dtype=np.int32), 16)
+    g, osum, opt, _ = run_both(4, 2, tr, P(policy=policy), cells=cells, n_cells=16)
+    compare_summaries(g.summaries, osum)
+    compare_tasks(tr, g, opt, osum)
+    # per-cell integer aggregates equal the oracle's per-trace sums
+    for c in range(16):
+        sel = cells == c
+        assert g.cells["n_slo_met"][c] == osum["n_slo_met"][sel].sum()
+        assert g.cells["n_tasks"][c] == osum["n_tasks"][sel].sum()
+
+
+# ---------------------------------------------------------------- variants
+@pytest.mark.parametrize("N,S", [(1, 1), (1, 3), (3, 2), (5, 3), (8, 1), (16, 16), (33, 2), (100, 2)])
+def test_shapes(N, S):
+    tr = workload.generate(workload.tiny_spec(rate=40.0, n_inf=120), 3, seed_base=7)
+    check(N, S, tr, P())
+    if N >= 2:
+        check(N, S, tr, P(policy=lemix.LMX_SEPARATE, alpha=0.3))
+    check(N, S, tr, P(policy=lemix.LMX_RR))
+
+
+@pytest.mark.parametrize("kw", [dict(deprioritize=0), dict(slo_mode=1, slo_const=0.05), dict(lc0=0.3989),
+                                dict(tau=0.01), dict(tau=-0.02), dict(lambda1=2.0, lambda2=0.5),
+                                dict(lambda2=0.0), dict(sigma_floor=25.0), dict(slo_mult=1.5)])
+def test_params(kw):
+    tr = workload.generate(workload.sweep_spec(120.0), 8, seed_base=21)
+    check(4, 2, tr, P(**kw))
+
+
+def test_edge_traces():
+    tr = workload.from_lists([
+        [],                                                  # empty
+        [(0.0, 16, 1, 0)],                                   # one inference task
+        [(0.0, 300, 2, 1)],                                  # one training task
+        [(1.0, 64, 1, 0), (1.0, 64, 1, 0), (1.0, 64, 1, 0)],  # equal arrivals
+        [(0.0, 100, 1, 1)] * 5,                              # training only, continuous
+        [(0.5 * k, 2048, 255, k % 2) for k in range(40)],    # maximal w = 255 * 2048^2
+        [(0.0, 1, 1, 0), (0.0, 1, 1, 1), (0.0, 1, 1, 0)],    # inference/training tie at t = 0
+    ])
+    for pol in POLICIES:
+        check(4, 2, tr, P(policy=pol))
+        check(1, 2, tr, P(policy=pol)) if pol != lemix.LMX_SEPARATE else None
+
+
+def test_queue_capacity_overflow():
+    tr = workload.generate(workload.sweep_spec(160.0), 8, seed_base=3)
+    g, osum, _ = check(4, 2, tr, P(qcap=3))
+    assert (osum["status"] == 6).any(), "fixture should overflow qcap=3"
+    assert g.status == 6
+
+
+def test_invalid_input_detected():
+    tr = workload.generate(workload.tiny_spec(), 3, seed_base=2)
+    tr.lbk[tr.offsets[1] + 5] = workload.pack(0, 1, 0)        # length 0 in trace 1
+    g, osum, _ = check(4, 2, tr, P())
+    assert osum["status"][1] == 1 and g.summaries["status"][1] == 1
+    assert g.status == 1 and "trace 1" in g.error
+
+
+# ---------------------------------------------------------------- large cluster
+def test_large_cluster_trace():
+    N, S = 64, 8
+    tr = workload.generate(workload.large_spec(rate=1600.0, n_inf=20000), 2, seed_base=5)
+    check(N, S, tr, P(qcap=1024))
