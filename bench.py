@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the LeMix placement step on B200 (BASELINE.json metric:
+scheduling decisions/s and traces/s at 1/2/4/8 GPUs, % of roofline).
+
+Workload (config.workload): the Monte Carlo scaling config -- per GPU 65,536
+independent seeded traces of 10k inference requests + 10k training
+micro-batches (20k decisions each; half Poisson, half bursty Gamma CV = 3
+arrivals, LogNormal lengths), N = 4 nodes x S = 2 stages, Llama-8B profile,
+LeMix policy, summary-only outputs.  One step = one lmx_run over all traces
+(every decision of every trace) + the per-cell summary reduction (+ the NCCL
+all-reduce of the cell aggregates when N > 1).  Weak scaling: each rank owns
+its own 65,536 traces (seeds offset by rank), no data-path collective.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lemix|reference]
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_NODES, N_STAGES = 4, 2
+METRIC = "scheduling decisions/sec"
+UNIT = "decisions/s"
+
+# Algorithmic fp64 operations (IEEE add/sub/mul/div/sqrt/compare) per oracle
+# event, read off the canonical expression sheet.
+OP_WEIGHTS = {
+    "decisions": 1 + 2 + 1,      # event select compare; t_last MAX + output fold; release/TTFT MAX
+    "stage_iters": 6,            # dF mul, start MAX, end add, II: sub, sub, add
+    "scan_consumed": 4,          # fit compare, MAX, end add, offset compare (+ GC compare at s=0 ~ +0.5)
+    "scan_break": 1,             # fit compare
+    "offset_adds": 2,            # eta_b*w mul, add
+    "alg1_calls": 4 + 4 + 1,     # Eq.1 (div, sub, sub, MAX), Eq.3 (mul, add, mul, div), arg-best compare
+    "lc_exp": 3 + 34 + 1,        # d sub, d*d, *k; exp_neg (cmp, mul, rint, mul, sub, mul, sub, 13x(mul,add), scale); c*
+    "commits_train": 3 * N_STAGES + 2 * N_STAGES,   # backward MAX/mul/add per stage; busy += dB
+    "eq4_checks": 3 * N_NODES + 2 * N_STAGES + 3,   # per node add/mul/MIN; tau_R; sub + compare
+    "version_scan": 1,
+}
+# per-decision commit work independent of the counters: busy += dF (2S), stats (div, sqrt, div, MAX,
+# mul, div, mul, div = 8), inference TTFT/SLO (sub, add, tau_R 2S+1, compare) ~ counted as 2S+4
+COMMIT_OPS = 2 * N_STAGES + 8 + (2 * N_STAGES + 4) // 2
+
+
+def ops_per_decision(counters: dict) -> float:
+    total = sum(OP_WEIGHTS[k] * counters[k] for k in OP_WEIGHTS)
+    total += COMMIT_OPS * counters["decisions"]
+    return total / max(1, counters["decisions"])
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "hw_power_brake_slowdown": 0x80, "sw_power_cap": 0x4}
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._th = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for k, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._th:
+            self._th.join()
+
+    def report(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def oracle_sample(traces, n_threads, policy=0):
+    """Run the oracle as it stands over a trace batch, threads over slices."""
+    import concurrent.futures as cf
+
+    import oracle
+    import workload
+    ef, eb = workload.profile(N_NODES, N_STAGES)
+    T = traces.n_traces
+    bounds = [(T * k // n_threads, T * (k + 1) // n_threads) for k in range(n_threads)]
+    bounds = [b for b in bounds if b[1] > b[0]]
+
+    def work(b):
+        sub = traces.subset(range(b[0], b[1]))
+        return oracle.run_batch(ef, eb, N_NODES, N_STAGES, sub, oracle.OracleParams(policy=policy), outputs=False)
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(len(bounds)) as ex:
+        res = list(ex.map(work, bounds))
+    dt = time.perf_counter() - t0
+    sums = np.concatenate([r[0] for r in res])
+    counters = {k: sum(r[2][k] for r in res) for k in res[0][2]}
+    counters["max_qlen"] = max(r[2]["max_qlen"] for r in res)
+    return sums, counters, dt, len(bounds)
+
+
+def sample_indices(n_traces, n):
+    """n trace indices, half from each (Poisson / bursty) half."""
+    half = n_traces // 2
+    a = np.linspace(0, half - 1, n // 2).astype(np.int64)
+    b = np.linspace(half, n_traces - 1, n - n // 2).astype(np.int64)
+    return np.unique(np.concatenate([a, b]))
+
+
+def config_dict(args, world):
+    per = args.n_inf + args.n_train
+    return {"workload": (f"mc: {args.traces} seeded traces/GPU x {args.n_inf} inference requests + "
+                         f"{args.n_train} training micro-batches (half Poisson, half bursty CV=3), "
+                         f"LogNormal lengths, N={N_NODES} nodes x S={N_STAGES} stages, Llama-8B profile, "
+                         f"LeMix, summary-only"),
+            "traces_per_gpu": args.traces, "tasks_per_trace": per, "n_nodes": N_NODES, "n_stages": N_STAGES,
+            "policy": "lemix", "qcap": args.qcap,
+            "l2": f"inputs {args.traces * per * 12 / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)",
+            "parallelism": f"dp{world} (independent traces sharded, one NCCL summary all-reduce)"}
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the CPU oracle as it stands on the host cores."""
+    if rank != 0:
+        return
+    import workload
+    n = args.ref_traces
+    # a bounded sample of the same workload: the seeds of the GPU arm's first
+    # Poisson traces and first bursty traces
+    half_seeds = n // 2
+    parts = [workload.generate(workload.mc_spec(False, args.n_inf, args.n_train), half_seeds, args.seed),
+             workload.generate(workload.mc_spec(True, args.n_inf, args.n_train), n - half_seeds,
+                               args.seed + args.traces // 2)]
+    tr = workload.concat(parts)
+    threads = os.cpu_count() or 1
+    times = []
+    for k in range(args.warmup + args.steps):
+        _, counters, dt, used = oracle_sample(tr, threads)
+        if k >= args.warmup:
+            times.append(dt)
+    decisions = tr.n_tasks
+    step = statistics.mean(times)
+    value = decisions / step
+    sample = f"{n} traces ({n * (args.n_inf + args.n_train)} decisions) of the mc workload per step"
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args, world),
+            "traces_per_s": n / step,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="lemix", choices=["lemix", "reference"])
+    ap.add_argument("--traces", type=int, default=65536, help="traces per GPU")
+    ap.add_argument("--n-inf", type=int, default=10000)
+    ap.add_argument("--n-train", type=int, default=10000)
+    ap.add_argument("--qcap", type=int, default=512)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-traces", type=int, default=0, help="oracle sample size (0 = auto)")
+    ap.add_argument("--ref-traces", type=int, default=256)
+    ap.add_argument("--check-traces", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import workload
+    from paper_2507_21276_b200 import lemix
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU path)")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- inputs: pinned host memory, then resident in HBM ----------------
+    T = args.traces
+    per = args.n_inf + args.n_train
+    M = T * per
+    t_gen = time.perf_counter()
+    arrival_h = torch.empty(M, dtype=torch.float64, pin_memory=True)
+    lbk_h = torch.empty(M, dtype=torch.int32, pin_memory=True)
+    tr = workload.mc_traces(T, seed_base=args.seed + rank * T, n_inf=args.n_inf, n_train=args.n_train,
+                            out=(arrival_h.numpy(), lbk_h.numpy().view(np.uint32)), with_out_len=False)
+    t_gen = time.perf_counter() - t_gen
+    stream = torch.cuda.current_stream()
+    arrival_d = arrival_h.to("cuda", non_blocking=True)
+    lbk_d = lbk_h.to("cuda", non_blocking=True)
+    torch.cuda.synchronize()
+
+    ef, eb = workload.profile(N_NODES, N_STAGES)
+    params = lemix.Params(policy=lemix.LMX_LEMIX, qcap=args.qcap)
+    ctx = lemix.Context(local_rank, stream.cuda_stream)
+    ctx.lmx_load_profile(N_NODES, N_STAGES, ef, eb)
+    ctx.lmx_load_traces(tr.offsets, tr.n_inf, arrival_d, lbk_d, mem=lemix.LMX_DEVICE)
+    ctx.lmx_set_params(params)
+    ctx.lmx_set_outputs(False)
+
+    comm = None
+    if world > 1:
+        obj = [lemix.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = lemix.nccl_comm_init(world, obj[0], rank, local_rank)
+
+    def step():
+        ctx.lmx_run()
+        if comm is not None:
+            ctx.lmx_allreduce_cells(comm)
+        st = ctx.lmx_sync()
+        if st != lemix.LMX_OK:
+            raise SystemExit(f"bench: trace failure {lemix.STATUS_NAMES[st]}: {ctx.last_error()}")
+        return ctx.lmx_get_timing()
+
+    for _ in range(args.warmup):
+        step()
+
+    # ---------------- timed region: device-resident inputs ----------------
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+    launches = 0
+    sampler = ClockSampler(local_rank)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            k_ms, r_ms, n_l = step()
+            kernel_ms.append(k_ms)
+            launches += n_l
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    t_max = torch.tensor([elapsed], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    elapsed = float(t_max.item())
+    step_s = elapsed / args.steps
+    decisions_per_step = M * world
+    value = decisions_per_step / step_s
+    cells = ctx.lmx_get_cells(1)
+    sums_gpu = ctx.lmx_get_summaries(T)
+
+    # ---------------- e2e: host (pinned) inputs through the public API ----------------
+    e2e = None
+    if not args.no_e2e:
+        h2d = M * 12 + (T + 1) * 8 + T * 4
+        d2h = lemix.CELL_DTYPE.itemsize
+        arr_np = arrival_h.numpy()
+        lbk_np = lbk_h.numpy().view(np.uint32)
+
+        def e2e_step():
+            ctx.lmx_load_traces(tr.offsets, tr.n_inf, arr_np, lbk_np, mem=lemix.LMX_HOST)
+            ctx.lmx_run()
+            if comm is not None:
+                ctx.lmx_allreduce_cells(comm)
+            st = ctx.lmx_sync()
+            if st != lemix.LMX_OK:
+                raise SystemExit(f"bench e2e: {ctx.last_error()}")
+            return ctx.lmx_get_cells(1)
+
+        e2e_step()
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        te = torch.tensor([e0.elapsed_time(e1) / 1e3], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": decisions_per_step / (float(te.item()) / args.steps), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "path": "lmx_load_traces(HOST, pinned) -> lmx_run -> lmx_sync -> lmx_get_cells"}
+
+    # ---------------- oracle: sampled parity + cpu_baseline + op counts ----------------
+    cpu = None
+    parity = None
+    roofline = None
+    if rank == 0:
+        import oracle  # noqa: F401  (test infrastructure: cpu_baseline leg only)
+        threads = os.cpu_count() or 1
+        n_cpu = args.cpu_traces or max(2 * threads, 16 * threads)
+        n_cpu = min(n_cpu, T)
+        idx = sample_indices(T, n_cpu)
+        sub = tr.subset(idx)
+        osum, counters, dt, used = oracle_sample(sub, threads)
+        # sampled parity in the bench's own launch configuration (summary-only run)
+        gs = sums_gpu[idx]
+        same_int = all(np.array_equal(gs[k], osum[k]) for k in lemix.SUMMARY_INT)
+        same_f = all(np.array_equal(gs[k].view(np.int64), osum[k].view(np.int64)) for k in lemix.SUMMARY_F64)
+        parity = {"sampled_traces": int(len(idx)), "integers_exact": bool(same_int), "fp64_bitwise": bool(same_f)}
+        if world == 1 and not args.no_cpu:
+            cpu = {"value": sub.n_tasks / dt, "unit": UNIT, "cores": used, "kind": "oracle",
+                   "sample": f"{len(idx)} traces of the same workload ({sub.n_tasks} decisions), "
+                             f"{used} threads over trace slices, {dt:.1f} s wall"}
+        opd = ops_per_decision(counters)
+        peaks, peak_src = measured_peaks()
+        sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        n_sm = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        peak_tflops = 64 * n_sm * sm_mhz * 1e6 / 1e12     # fp64 lanes/clk/SM x SMs x clock
+        k_s = statistics.mean(kernel_ms) / 1e3
+        achieved = opd * M / k_s / 1e12
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                tj = json.load(f)
+            if tj.get("traces") == T and tj.get("tasks_per_trace") == per:
+                traffic = tj.get("dram_bytes_per_launch")
+        except OSError:
+            pass
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
+                    "frac": achieved / peak_tflops, "traffic": traffic,
+                    "kernel": "lmx::event_loop_kernel<2,1>",
+                    "note": (f"fp64 pipe: {opd:.1f} algorithmic fp64 ops/decision (oracle counters x DESIGN.md "
+                             f"weights) x {M} decisions / {k_s * 1e3:.1f} ms mean kernel time; peak = 64 "
+                             f"DP lanes/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz ({peak_src} clock); "
+                             f"HBM bound {M * 12 / k_s / 1e9:.0f} GB/s of {peaks.get('hbm_gbs')}"),
+                    "max_queue_depth_sample": counters["max_qlen"]}
+
+    if rank == 0:
+        grid, block, lanes, smem = ctx.lmx_get_geometry()
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config_dict(args, world),
+                "traces_per_s": T * world / step_s,
+                "kernel_ms_mean": statistics.mean(kernel_ms),
+                "gpu_launches": launches,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.report(),
+                "parity": parity,
+                "summary_check": {"n_failed_traces": int(cells["n_failed"][0]),
+                                  "slo_attainment_mean": float(cells["sum_slo_attainment"][0] / max(1, cells["n_traces"][0] - cells["n_failed"][0])),
+                                  "throughput_mean": float(cells["sum_throughput"][0] / max(1, cells["n_traces"][0] - cells["n_failed"][0]))},
+                "geometry": {"grid": grid, "block": block, "lanes_per_trace": lanes, "smem": smem},
+                "context": {"paper_table2": "LeMix EP+RA 0.154 ms/decision (~6.5e3 decisions/s, Python, A100 host, "
+                                            "Llama-70B 50 rps) -- different machine/workload, not a target"},
+                "gen_s": round(t_gen, 1)}
+        print(json.dumps(line), flush=True)
+
+    ctx.close()
+    if comm is not None:
+        lemix.nccl_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -110,7 +110,8 @@ class Traces:
     def trace(self, t: int) -> "Traces":
         o0, o1 = int(self.offsets[t]), int(self.offsets[t + 1])
         return Traces(np.array([0, o1 - o0], np.int64), self.n_inf[t:t + 1].copy(),
-                      self.arrival[o0:o1], self.lbk[o0:o1], self.out_len[o0:o1])
+                      self.arrival[o0:o1], self.lbk[o0:o1],
+                      None if self.out_len is None else self.out_len[o0:o1])
 
     def subset(self, idx) -> "Traces":
         return concat([self.trace(int(t)) for t in idx])
@@ -143,7 +144,7 @@ def generate(spec: WorkloadSpec, n_traces: int, seed_base: int = 1, n_threads: i
     if n_threads is None:
         n_threads = os.cpu_count() or 1
     rc = lib.wl_generate(ctypes.byref(spec._c()), n_traces, seed_base, arrival.ctypes.data,
-                         lbk.ctypes.data, out_len.ctypes.data, n_threads)
+                         lbk.ctypes.data, None if out_len is None else out_len.ctypes.data, n_threads)
     if rc != 0:
         raise ValueError(f"invalid workload spec: {spec}")
     offsets = np.arange(n_traces + 1, dtype=np.int64) * per
@@ -161,7 +162,7 @@ def concat(parts) -> Traces:
         base += sz
     return Traces(np.concatenate(offsets), np.concatenate([p.n_inf for p in parts]).astype(np.int32),
                   np.concatenate([p.arrival for p in parts]), np.concatenate([p.lbk for p in parts]),
-                  np.concatenate([p.out_len for p in parts]))
+                  None if any(p.out_len is None for p in parts) else np.concatenate([p.out_len for p in parts]))
 
 
 def from_lists(traces) -> Traces:
@@ -234,19 +235,25 @@ def mc_spec(bursty=False, n_inf=10000, n_train=10000, rate=50.0):
                         bursty=bursty, cv=3.0)
 
 
-def mc_traces(n_traces=65536, seed_base=1, n_inf=10000, n_train=10000, n_threads=None) -> Traces:
+def mc_traces(n_traces=65536, seed_base=1, n_inf=10000, n_train=10000, n_threads=None, out=None,
+              with_out_len=True) -> Traces:
     """Monte Carlo config: the first half Poisson, the second half bursty
-    (Gamma CV = 3), seeds seed_base + t."""
+    (Gamma CV = 3), seeds seed_base + t.  `out` = (arrival, lbk) buffers to
+    fill (e.g. pinned host memory)."""
     half = n_traces // 2
     per = n_inf + n_train
     m = per * n_traces
-    arrival = np.empty(m, np.float64)
-    lbk = np.empty(m, np.uint32)
-    out_len = np.empty(m, np.uint32)
+    if out is None:
+        arrival = np.empty(m, np.float64)
+        lbk = np.empty(m, np.uint32)
+    else:
+        arrival, lbk = out
+    out_len = np.empty(m, np.uint32) if with_out_len else None
+    ol = (lambda a, b: None) if out_len is None else (lambda a, b: out_len[a:b])
     generate(mc_spec(False, n_inf, n_train), half, seed_base, n_threads,
-             out=(arrival[:half * per], lbk[:half * per], out_len[:half * per]))
+             out=(arrival[:half * per], lbk[:half * per], ol(0, half * per)))
     generate(mc_spec(True, n_inf, n_train), n_traces - half, seed_base + half, n_threads,
-             out=(arrival[half * per:], lbk[half * per:], out_len[half * per:]))
+             out=(arrival[half * per:], lbk[half * per:], ol(half * per, m)))
     offsets = np.arange(n_traces + 1, dtype=np.int64) * per
     return Traces(offsets, np.full(n_traces, n_inf, np.int32), arrival, lbk, out_len)
 

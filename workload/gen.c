@@ -119,7 +119,9 @@ static void gen_trace(const wl_spec *sp, uint64_t seed, double *arr, uint32_t *l
         arr[k] = t;
         lbk[k] = pack(lognormal_len(&r, sp->len_inf_median, sp->len_inf_sigma, sp->len_min, sp->len_max),
                       sp->batch_inf, 0);
-        if (out_len) out_len[k] = (uint32_t)lognormal_len(&r, sp->out_median, sp->out_sigma, 1, 2048);
+        /* always drawn, so the stream does not depend on whether it is kept */
+        uint32_t ol = (uint32_t)lognormal_len(&r, sp->out_median, sp->out_sigma, 1, 2048);
+        if (out_len) out_len[k] = ol;
     }
     t = 0.0;
     for (int64_t k = 0; k < sp->n_train; ++k) {
