@@ -68,4 +68,12 @@ int event_loop_occupancy(const KParams &p, int *err);
 int launch_event_loop(const KParams &p, int grid, void *stream);
 int launch_cells(const CellParams &c, void *stream);
 
+// lane-per-trace variant (lemix_lane.cu): N <= 8, S <= 4, N*S small
+bool lane_supported(int N, int S);
+int lane_smem_bytes(const KParams &p);
+int lane_block_threads();
+int lane_nodes_bucket(int N);
+int lane_occupancy(const KParams &p, int *err);
+int launch_lane_loop(const KParams &p, int grid, void *stream);
+
 }  // namespace lmx

@@ -28,17 +28,11 @@ namespace lmx {
 namespace {
 
 constexpr int kBlock = 128;                 // 4 warps per CTA
-constexpr double kInf = __builtin_huge_val();
-constexpr double kSqrt2Pi = 0x1.40d931ff62705p+1;
-
-__device__ __forceinline__ int task_len(uint32_t v) { return (int)(v & 0xFFFu); }
-__device__ __forceinline__ int task_batch(uint32_t v) { return (int)((v >> 12) & 0xFFu); }
-// C * l^2, exact in int64 and as a double (< 2^31)
-__device__ __forceinline__ double task_w(uint32_t v)
-{
-    const long long l = task_len(v), c = task_batch(v);
-    return (double)(c * l * l);
-}
+using dev::kInf;
+using dev::kSqrt2Pi;
+using dev::task_batch;
+using dev::task_len;
+using dev::task_w;
 
 template <int SMAX, int NPL>
 __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
@@ -69,9 +63,15 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
     const long long gtile = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> log2T;
     const long long K = (long long)p.kmask + 1;
 
-    long long rbase[NPL];   // first ring entry of this lane's nodes
+    // the Q_train ring of each node this lane owns
+    double2 *rbe[NPL];
+    double *rwv[NPL];
 #pragma unroll
-    for (int jj = 0; jj < NPL; ++jj) rbase[jj] = (gtile * p.npad + (tl + jj * T)) * K;
+    for (int jj = 0; jj < NPL; ++jj) {
+        const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
+        rbe[jj] = p.ring_be + rbase * S;
+        rwv[jj] = p.ring_w + rbase;
+    }
 
     // ---- per-trace (tile-replicated) state ----
     bool active = false, finished = false;
@@ -86,61 +86,66 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
     // ---- per-node state of this lane's slots (registers) ----
     double P[NPL][SMAX], LB[NPL][SMAX], busy[NPL][SMAX];
     double aprev[NPL], mu[NPL], kk[NPL], cc[NPL];
-    int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL], ntr[NPL];
+    int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL], ntr[NPL], vp[NPL];
+    int sk[NPL][SMAX];   // stale-prefix pointers (see dev::plan)
     long long sl[NPL], sl2[NPL];
 
+    // Control flow inside the loop is structured (no continue/break out of a
+    // branch) so tiles that took different branches reconverge right after it.
     while (!__all_sync(0xffffffffu, finished)) {
-        if (finished) continue;
-        if (!active) {
+        if (!finished && !active) {
             // ---- claim the next trace ----
             unsigned long long tt = 0;
             if (tl == 0) tt = atomicAdd(p.work, 1ull);
             tt = __shfl_sync(tmask, tt, tbase);
             if (tt >= (unsigned long long)p.n_traces) {
                 finished = true;
-                continue;
-            }
-            t = (long long)tt;
-            o = p.offsets[t];
-            const int len = (int)(p.offsets[t + 1] - o);
-            nI = p.n_inf[t];
-            nT = len - nI;
-            i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
-            status = LMX_OK;
-            err_task = 0;
-            err_code = kErrNone;
-            n_slo = sum_ver = n_def = 0;
-            sum_ttft = 0.0;
-            t_last = -kInf;
-            a_last_inf = -kInf;
-            if (nI > 0) { a_inf = __ldg(p.arrival + o); v_inf = __ldg(p.lbk + o); }
-            if (nI > 1) { a_inf2 = __ldg(p.arrival + o + 1); v_inf2 = __ldg(p.lbk + o + 1); }
-            if (nT > 0) { a_tr = __ldg(p.arrival + o + nI); v_tr = __ldg(p.lbk + o + nI); }
-            if (nT > 1) { a_tr2 = __ldg(p.arrival + o + nI + 1); v_tr2 = __ldg(p.lbk + o + nI + 1); }
-            r = (nT > 0) ? a_tr : kInf;
-            t_first = kInf;
-            if (nI > 0) t_first = dev::dmin(t_first, a_inf);
-            if (nT > 0) t_first = dev::dmin(t_first, a_tr);
+            } else {
+                t = (long long)tt;
+                o = p.offsets[t];
+                const int len = (int)(p.offsets[t + 1] - o);
+                nI = p.n_inf[t];
+                nT = len - nI;
+                i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
+                status = LMX_OK;
+                err_task = 0;
+                err_code = kErrNone;
+                n_slo = sum_ver = n_def = 0;
+                sum_ttft = 0.0;
+                t_last = -kInf;
+                a_last_inf = -kInf;
+                if (nI > 0) { a_inf = __ldg(p.arrival + o); v_inf = __ldg(p.lbk + o); }
+                if (nI > 1) { a_inf2 = __ldg(p.arrival + o + 1); v_inf2 = __ldg(p.lbk + o + 1); }
+                if (nT > 0) { a_tr = __ldg(p.arrival + o + nI); v_tr = __ldg(p.lbk + o + nI); }
+                if (nT > 1) { a_tr2 = __ldg(p.arrival + o + nI + 1); v_tr2 = __ldg(p.lbk + o + nI + 1); }
+                r = (nT > 0) ? a_tr : kInf;
+                t_first = kInf;
+                if (nI > 0) t_first = dev::dmin(t_first, a_inf);
+                if (nT > 0) t_first = dev::dmin(t_first, a_tr);
 #pragma unroll
-            for (int jj = 0; jj < NPL; ++jj) {
-                hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = ntr[jj] = 0;
-                sl[jj] = sl2[jj] = 0;
-                aprev[jj] = mu[jj] = kk[jj] = cc[jj] = 0.0;
+                for (int jj = 0; jj < NPL; ++jj) {
+                    hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = ntr[jj] = vp[jj] = 0;
+                    sl[jj] = sl2[jj] = 0;
+                    aprev[jj] = mu[jj] = kk[jj] = cc[jj] = 0.0;
 #pragma unroll
-                for (int s = 0; s < SMAX; ++s) { P[jj][s] = 0.0; LB[jj][s] = -kInf; busy[jj][s] = 0.0; }
+                    for (int s = 0; s < SMAX; ++s) {
+                        P[jj][s] = 0.0;
+                        LB[jj][s] = -kInf;
+                        busy[jj][s] = 0.0;
+                        sk[jj][s] = 0;
+                    }
+                }
+                if (p.policy == LMX_SEPARATE && N == 1 && nI > 0 && nT > 0) {
+                    status = LMX_EINVAL;
+                    err_code = kErrSeparateN1;
+                }
+                active = true;
             }
-            if (p.policy == LMX_SEPARATE && N == 1 && nI > 0 && nT > 0) {
-                status = LMX_EINVAL;
-                err_code = kErrSeparateN1;
-            }
-            active = true;
         }
+        if (!active) continue;   // (finished lanes only: back to the warp vote)
 
-        bool done_trace = (status != LMX_OK) || (i >= nI && j >= nT);
-        if (!done_trace && ++iters > 2 * (nI + nT) + 2) {
-            status = LMX_EBUDGET;
-            done_trace = true;
-        }
+        if (status == LMX_OK && (i < nI || j < nT) && ++iters > 2 * (nI + nT) + 2) status = LMX_EBUDGET;
+        const bool done_trace = (status != LMX_OK) || (i >= nI && j >= nT);
 
         if (done_trace) {
             // ---- per-trace metrics, node folds in node order ----
@@ -174,11 +179,11 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s) {
                         if (s < S) {
-                            double b = 0.0;
+                            double bv = 0.0;
 #pragma unroll
                             for (int jj = 0; jj < NPL; ++jj)
-                                if (jj == jn) b = busy[jj][s];
-                            U = U + dev::shfl_d(tmask, b, src);
+                                if (jj == jn) bv = busy[jj][s];
+                            U = U + dev::shfl_d(tmask, bv, src);
                         }
                     }
                     double sd = (c > 0) ? sqrt((double)v2) / (double)c : 0.0;
@@ -201,30 +206,23 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
                 }
             }
             active = false;
-            continue;
-        }
-
-        // ---- a1: event selection (ties -> inference) ----
-        const double t_inf = (i < nI) ? a_inf : kInf;
-        const bool is_train = !(t_inf <= r);
-        double now;
-        uint32_t v;
-        if (!is_train) {
-            now = t_inf;
-            v = v_inf;
         } else {
-            now = r;
-            v = v_tr;
-            // ---- a2: Eq. 4 queue-level deprioritisation against the next
-            // enqueued inference task (R-14/R-15) ----
-            if (p.policy == LMX_LEMIX && p.deprioritize && i < nI) {
+            // ---- a1: event selection (ties -> inference) ----
+            const double t_inf = (i < nI) ? a_inf : kInf;
+            const bool is_train = !(t_inf <= r);
+            const double now = is_train ? r : t_inf;
+            const uint32_t v = is_train ? v_tr : v_inf;
+            bool deferred = false;
+            if (is_train && p.policy == LMX_LEMIX && p.deprioritize && i < nI) {
+                // ---- a2: Eq. 4 queue-level deprioritisation against the next
+                // enqueued inference task (R-14/R-15) ----
                 const double wn = task_w(v_inf);
                 double m = kInf;
 #pragma unroll
                 for (int jj = 0; jj < NPL; ++jj) {
                     const int n = tl + jj * T;
                     if (n < N) {
-                        const double latest = hasp[jj] ? P[jj][S - 1] : -kInf;
+                        const double latest = hasp[jj] ? dev::last_of(P[jj], S) : -kInf;
                         m = dev::dmin(m, latest + s_ef[n * S + S - 1] * wn);
                     }
                 }
@@ -237,274 +235,238 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
                     for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * wn;
                     tauR = p.slo_mult * acc;
                 }
-                if ((m - t_inf) > tauR) {
+                deferred = (m - t_inf) > tauR;
+                if (deferred) {
                     r = t_inf;          // move behind the next inference task
                     cur_defer++;
                     n_def++;
-                    continue;
                 }
             }
-        }
-        const int task = is_train ? nI + j : i;
-
-        // ---- input validation of the task being placed ----
-        {
-            const double arr = is_train ? a_tr : a_inf;
-            int code = kErrNone;
-            if (v >> 21) code = kErrBits;
-            else if (task_len(v) < 1 || task_len(v) > 2048) code = kErrLen;
-            else if (task_batch(v) < 1) code = kErrBatch;
-            else if ((int)((v >> 20) & 1u) != (int)is_train) code = kErrKind;
-            else if (!(arr >= 0.0 && arr < kInf)) code = kErrArrival;
-            else if (!is_train && arr < a_last_inf) code = kErrOrder;
-            int fx = 0;
-            if (p.policy == LMX_FIXED) {
-                fx = __ldg(p.fixed + o + task);
-                if (code == kErrNone && (fx < 0 || fx >= N)) code = kErrFixed;
-            }
-            if (code != kErrNone) {
-                status = LMX_EINVAL;
-                err_task = task;
-                err_code = code;
-                continue;
-            }
-        }
-
-        const double a = now;                    // dispatch time (R-2)
-        const double w = task_w(v);
-        const int l = task_len(v);
-
-        // ---- a9: baseline selectors ----
-        int chosen = -1;
-        if (p.policy == LMX_RR) {
-            chosen = rr % N;
-            rr++;
-        } else if (p.policy == LMX_SEPARATE) {
-            if (!(nI > 0 && nT > 0)) {
-                chosen = is_train ? (sep_t++ % N) : (sep_i++ % N);
-            } else if (is_train) {
-                chosen = (N - p.n_tr_sep) + (sep_t++ % p.n_tr_sep);
-            } else {
-                chosen = sep_i++ % (N - p.n_tr_sep);
-            }
-        } else if (p.policy == LMX_FIXED) {
-            chosen = __ldg(p.fixed + o + task);
-        }
-
-        // ---- a3-a7: Algorithm 1 + Eq. 1-3 for every candidate this lane owns ----
-        double en_s[NPL][SMAX];
-        double st0_s[NPL];
-        double f_best = 0.0;
-        int n_best = INT_MAX;
-#pragma unroll
-        for (int jj = 0; jj < NPL; ++jj) {
-            const int n = tl + jj * T;
-            st0_s[jj] = 0.0;
-#pragma unroll
-            for (int s = 0; s < SMAX; ++s) en_s[jj][s] = 0.0;
-            if (n < N && (p.policy == LMX_LEMIX || n == chosen)) {
-                const double *ef = s_ef + n * S;
-                const double *eb = s_eb + n * S;
-                // line 3: task_prev; a never-used node has a virtual predecessor (R-1)
-                double Pv[SMAX];
-                if (hasp[jj]) {
-#pragma unroll
-                    for (int s = 0; s < SMAX; ++s) Pv[s] = P[jj][s];
-                } else {
-                    double vv = a;
-#pragma unroll
-                    for (int s = 0; s < SMAX; ++s)
-                        if (s < S) { Pv[s] = vv; vv = vv + ef[s] * w; }
+            const int task = is_train ? nI + j : i;
+            if (!deferred) {
+                // ---- input validation of the task being placed ----
+                const double arr = is_train ? a_tr : a_inf;
+                int code = kErrNone;
+                if (v >> 21) code = kErrBits;
+                else if (task_len(v) < 1 || task_len(v) > 2048) code = kErrLen;
+                else if (task_batch(v) < 1) code = kErrBatch;
+                else if ((int)((v >> 20) & 1u) != (int)is_train) code = kErrKind;
+                else if (!(arr >= 0.0 && arr < kInf)) code = kErrArrival;
+                else if (!is_train && arr < a_last_inf) code = kErrOrder;
+                if (p.policy == LMX_FIXED && code == kErrNone) {
+                    const int fx = __ldg(p.fixed + o + task);
+                    if (fx < 0 || fx >= N) code = kErrFixed;
                 }
-                double II = 0.0, e = a;
-                int cur = 0, gc = 0;
-                const int qhead = qh[jj], qlen = qn[jj];
-#pragma unroll
-                for (int s = 0; s < SMAX; ++s) {                    // line 4
-                    if (s < S) {
-                        const double dF = ef[s] * w;
-                        double st = dev::dmax(e, Pv[s]);            // line 5
-                        double en = st + dF;                        // line 6
-                        double off = 0.0;                           // line 7
-                        while (cur < qlen) {                        // lines 8-9 (Q_temp = cursor)
-                            const long long idx = rbase[jj] + ((qhead + cur) & p.kmask);
-                            const double2 q = p.ring_be[idx * S + s];   // (start_b^s, end_b^s)
-                            if (en <= q.x) break;                   // lines 10-12: stays at the front
-                            st = dev::dmax(st, q.y);                // line 13
-                            en = st + dF;                           // line 14
-                            if (Pv[s] <= q.x) off = off + eb[s] * p.ring_w[idx];   // lines 15-16
-                            if (s == 0 && q.y <= now) gc = cur + 1; // lines 17-18 CheckExecuted
-                            cur++;
-                        }
-                        II = II + ((st - Pv[s]) - off);             // line 19
-                        en_s[jj][s] = en;
-                        if (s == 0) st0_s[jj] = st;
-                        e = en;
-                    }
+                if (code != kErrNone) {
+                    status = LMX_EINVAL;
+                    err_task = task;
+                    err_code = code;
                 }
-                // lines 17-18: executed entries leave Q_train^n (a head advance:
-                // end_b^1 is non-decreasing along the queue)
-                qh[jj] = qhead + gc;
-                qn[jj] = qlen - gc;
-                if (p.policy == LMX_LEMIX) {
-                    const double R = e - a;                                       // line 20
-                    const double a_last = hasp[jj] ? aprev[jj] : a;               // R-9
-                    const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
-                    const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
-                    double LC;                                                    // Eq. 2
-                    if (cnt[jj] < 2) {
-                        LC = p.lc0;
+            }
+            if (!deferred && status == LMX_OK) {
+                const double a = now;                    // dispatch time (R-2)
+                const double w = task_w(v);
+                const int l = task_len(v);
+
+                // ---- a9: baseline selectors ----
+                int chosen = -1;
+                if (p.policy == LMX_RR) {
+                    chosen = rr % N;
+                    rr++;
+                } else if (p.policy == LMX_SEPARATE) {
+                    if (!(nI > 0 && nT > 0)) {
+                        chosen = is_train ? (sep_t++ % N) : (sep_i++ % N);
+                    } else if (is_train) {
+                        chosen = (N - p.n_tr_sep) + (sep_t++ % p.n_tr_sep);
                     } else {
-                        const double d = (double)l - mu[jj];
-                        LC = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
+                        chosen = sep_i++ % (N - p.n_tr_sep);
                     }
-                    const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
-                    if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
+                } else if (p.policy == LMX_FIXED) {
+                    chosen = __ldg(p.fixed + o + task);
                 }
-            }
-        }
 
-        // ---- a8: arg-best over the tile: highest f, then lowest node index ----
-        int best;
-        if (p.policy == LMX_LEMIX) {
-            for (int off = T >> 1; off > 0; off >>= 1) {
-                const double f2 = dev::shfl_xor_d(tmask, f_best, off);
-                const int n2 = __shfl_xor_sync(tmask, n_best, off);
-                if (n2 != INT_MAX &&
-                    (n_best == INT_MAX || f2 > f_best || (f2 == f_best && n2 < n_best))) {
-                    f_best = f2;
-                    n_best = n2;
-                }
-            }
-            best = n_best;
-        } else {
-            best = chosen;
-        }
-
-        // ---- a10: commit on the owning lane ----
-        const int owner = tbase + (best & (T - 1));
-        const int jb = best >> log2T;
-        double c_done = 0.0, c_en0 = 0.0, c_enS = 0.0, c_st0 = 0.0;
-        int c_ver = 0, c_status = LMX_OK;
-        if (lane == owner) {
+                // ---- a3-a7: Algorithm 1 + Eq. 1-3 for every candidate this lane owns ----
+                double en_s[NPL][SMAX];
+                double st0_s[NPL];
+                double f_best = 0.0;
+                int n_best = INT_MAX;
 #pragma unroll
-            for (int jj = 0; jj < NPL; ++jj) {
-                if (jj == jb) {
-                    const double *ef = s_ef + best * S;
-                    const double *eb = s_eb + best * S;
+                for (int jj = 0; jj < NPL; ++jj) {
+                    const int n = tl + jj * T;
+                    st0_s[jj] = 0.0;
 #pragma unroll
-                    for (int s = 0; s < SMAX; ++s)
-                        if (s < S) {
-                            P[jj][s] = en_s[jj][s];
-                            busy[jj][s] = busy[jj][s] + ef[s] * w;
-                        }
-                    hasp[jj] = 1;
-                    aprev[jj] = a;
-                    c_en0 = en_s[jj][0];
-                    c_enS = en_s[jj][S - 1];
-                    c_st0 = st0_s[jj];
-                    if (is_train) {
-                        if (qn[jj] >= p.qcap) {
-                            c_status = LMX_EQCAP;
-                        } else {
-                            // backward planning, stages S..1
-                            const long long idx = rbase[jj] + ((qh[jj] + qn[jj]) & p.kmask);
-                            double x = c_enS;
-#pragma unroll
-                            for (int s = SMAX - 1; s >= 0; --s) {
-                                if (s < S) {
-                                    const double sb = dev::dmax(x, LB[jj][s]);
-                                    const double ebv = sb + eb[s] * w;
-                                    LB[jj][s] = ebv;
-                                    p.ring_be[idx * S + s] = make_double2(sb, ebv);
-                                    x = ebv;
-                                }
+                    for (int s = 0; s < SMAX; ++s) en_s[jj][s] = 0.0;
+                    if (n < N && (p.policy == LMX_LEMIX || n == chosen)) {
+                        double II;
+                        int gc;
+                        const int qhead = qh[jj], qlen = qn[jj];
+                        const dev::Ring q{rbe[jj], rwv[jj], p.kmask, S};
+                        dev::plan<SMAX>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
+                                        a, now, en_s[jj], st0_s[jj], II, gc);
+                        // lines 17-18: executed entries leave Q_train^n (a head advance:
+                        // end_b^1 is non-decreasing along the queue)
+                        qh[jj] = qhead + gc;
+                        qn[jj] = qlen - gc;
+                        if (p.policy == LMX_LEMIX) {
+                            const double R = dev::last_of(en_s[jj], S) - a;               // line 20
+                            const double a_last = hasp[jj] ? aprev[jj] : a;               // R-9
+                            const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
+                            const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
+                            double LC;                                                    // Eq. 2
+                            if (cnt[jj] < 2) {
+                                LC = p.lc0;
+                            } else {
+                                const double d = (double)l - mu[jj];
+                                LC = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
                             }
-                            p.ring_w[idx] = w;
-                            qn[jj]++;
+                            const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
+                            if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
+                        }
+                    }
+                }
+
+                // ---- a8: arg-best over the tile: highest f, then lowest node index ----
+                int best;
+                if (p.policy == LMX_LEMIX) {
+                    for (int off = T >> 1; off > 0; off >>= 1) {
+                        const double f2 = dev::shfl_xor_d(tmask, f_best, off);
+                        const int n2 = __shfl_xor_sync(tmask, n_best, off);
+                        if (n2 != INT_MAX &&
+                            (n_best == INT_MAX || f2 > f_best || (f2 == f_best && n2 < n_best))) {
+                            f_best = f2;
+                            n_best = n2;
+                        }
+                    }
+                    best = n_best;
+                } else {
+                    best = chosen;
+                }
+
+                // ---- a10: commit on the owning lane ----
+                const int owner = tbase + (best & (T - 1));
+                const int jb = best >> log2T;
+                double c_done = 0.0, c_en0 = 0.0, c_st0 = 0.0;
+                int c_ver = 0, c_status = LMX_OK;
+                if (lane == owner) {
+#pragma unroll
+                    for (int jj = 0; jj < NPL; ++jj) {
+                        if (jj == jb) {
+                            const double *ef = s_ef + best * S;
+                            const double *eb = s_eb + best * S;
+                            const dev::Ring q{rbe[jj], rwv[jj], p.kmask, S};
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
-                                if (s < S) busy[jj][s] = busy[jj][s] + eb[s] * w;
-                            ntr[jj]++;
-                            c_done = x;
+                                if (s < S) {
+                                    P[jj][s] = en_s[jj][s];
+                                    busy[jj][s] = busy[jj][s] + ef[s] * w;
+                                }
+                            hasp[jj] = 1;
+                            aprev[jj] = a;
+                            c_en0 = en_s[jj][0];
+                            c_st0 = st0_s[jj];
+                            c_done = dev::last_of(en_s[jj], S);
+                            if (is_train && qn[jj] >= p.qcap) {
+                                c_status = LMX_EQCAP;
+                            } else if (is_train) {
+                                // backward planning, stages S..1
+                                const int slot = (qh[jj] + qn[jj]) & p.kmask;
+                                double x = c_done;
+#pragma unroll
+                                for (int s = SMAX - 1; s >= 0; --s) {
+                                    if (s < S) {
+                                        const double sb = dev::dmax(x, LB[jj][s]);
+                                        const double ebv = sb + eb[s] * w;
+                                        LB[jj][s] = ebv;
+                                        rbe[jj][slot * S + s] = make_double2(sb, ebv);
+                                        x = ebv;
+                                    }
+                                }
+                                rwv[jj][slot] = w;
+                                qn[jj]++;
+#pragma unroll
+                                for (int s = 0; s < SMAX; ++s)
+                                    if (s < S) busy[jj][s] = busy[jj][s] + eb[s] * w;
+                                ntr[jj]++;
+                                c_done = x;
+                            } else {
+                                // version-at-inference: completed backwards form a prefix of
+                                // Q_train; start_f^1 of successive commits on a node is
+                                // non-decreasing, so the boundary pointer only moves forward.
+                                int k = vp[jj] > qh[jj] ? vp[jj] : qh[jj];
+                                const int tail = qh[jj] + qn[jj];
+                                while (k < tail && q.at(k, 0).y <= c_st0) k++;
+                                vp[jj] = k;
+                                c_ver = ntr[jj] - (tail - k);
+                            }
+                            if (c_status == LMX_OK) {
+                                dev::advance_skip<SMAX>(sk[jj], P[jj], S, q, qh[jj], qh[jj] + qn[jj]);
+                                cnt[jj]++;
+                                sl[jj] += l;
+                                sl2[jj] += (long long)l * l;
+                                if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (population mean / sigma)
+                                    const long long c = cnt[jj];
+                                    mu[jj] = (double)sl[jj] / (double)c;
+                                    const long long var = c * sl2[jj] - sl[jj] * sl[jj];
+                                    const double sigma = dev::dmax(sqrt((double)var) / (double)c, p.sigma_floor);
+                                    kk[jj] = 0.5 / (sigma * sigma);
+                                    cc[jj] = 1.0 / (sigma * kSqrt2Pi);
+                                }
+                            }
                         }
-                    } else {
-                        c_done = c_enS;
-                        // version-at-inference: completed training tasks on this
-                        // node at the forward start.  end_b^1 is non-decreasing
-                        // along the queue, so the completed ones form a prefix.
-                        int k = 0;
-                        while (k < qn[jj] &&
-                               p.ring_be[(rbase[jj] + ((qh[jj] + k) & p.kmask)) * S].y <= c_st0)
-                            k++;
-                        c_ver = ntr[jj] - (qn[jj] - k);
-                    }
-                    cnt[jj]++;
-                    sl[jj] += l;
-                    sl2[jj] += (long long)l * l;
-                    if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (population mean / sigma)
-                        const long long c = cnt[jj];
-                        mu[jj] = (double)sl[jj] / (double)c;
-                        const long long var = c * sl2[jj] - sl[jj] * sl[jj];
-                        const double sigma = dev::dmax(sqrt((double)var) / (double)c, p.sigma_floor);
-                        kk[jj] = 0.5 / (sigma * sigma);
-                        cc[jj] = 1.0 / (sigma * kSqrt2Pi);
                     }
                 }
-            }
-        }
-        c_done = dev::shfl_d(tmask, c_done, owner);
-        c_en0 = dev::shfl_d(tmask, c_en0, owner);
-        c_enS = dev::shfl_d(tmask, c_enS, owner);
-        c_st0 = dev::shfl_d(tmask, c_st0, owner);
-        c_ver = __shfl_sync(tmask, c_ver, owner);
-        c_status = __shfl_sync(tmask, c_status, owner);
-        if (c_status != LMX_OK) {
-            status = c_status;
-            continue;
-        }
-
-        // ---- a11: outputs + per-trace folds ----
-        if (tl == 0 && p.node_defer) {
-            const unsigned dsat = is_train ? (unsigned)min(cur_defer, 0xFFFF) : 0u;
-            p.node_defer[o + task] = (uint32_t)best | (dsat << 16);
-            p.decision_idx[o + task] = step;
-            p.completion[o + task] = c_done;
-            p.start_f1[o + task] = c_st0;
-        }
-        t_last = dev::dmax(t_last, c_done);
-        step++;
-        if (is_train) {
-            j++;
-            cur_defer = 0;
-            a_tr = a_tr2;
-            v_tr = v_tr2;
-            if (j + 1 < nT) {
-                a_tr2 = __ldg(p.arrival + o + nI + j + 1);
-                v_tr2 = __ldg(p.lbk + o + nI + j + 1);
-            }
-            // next release: max(a_min, this task's S1 forward end)
-            r = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
-        } else {
-            const double ttft = c_enS - a;         // R from arrival
-            sum_ttft = sum_ttft + ttft;
-            double tauR;
-            if (p.slo_mode == 1) {
-                tauR = p.slo_const;
-            } else {
-                double acc = 0.0;
-                for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * w;
-                tauR = p.slo_mult * acc;
-            }
-            if (ttft <= tauR) n_slo++;              // SLO: TTFT <= 5x forward latency
-            sum_ver += c_ver;
-            a_last_inf = a;
-            i++;
-            a_inf = a_inf2;
-            v_inf = v_inf2;
-            if (i + 1 < nI) {
-                a_inf2 = __ldg(p.arrival + o + i + 1);
-                v_inf2 = __ldg(p.lbk + o + i + 1);
+                c_done = dev::shfl_d(tmask, c_done, owner);
+                c_en0 = dev::shfl_d(tmask, c_en0, owner);
+                c_st0 = dev::shfl_d(tmask, c_st0, owner);
+                c_ver = __shfl_sync(tmask, c_ver, owner);
+                c_status = __shfl_sync(tmask, c_status, owner);
+                if (c_status != LMX_OK) {
+                    status = c_status;
+                } else {
+                    // ---- a11: outputs + per-trace folds ----
+                    if (tl == 0 && p.node_defer) {
+                        const unsigned dsat = is_train ? (unsigned)min(cur_defer, 0xFFFF) : 0u;
+                        p.node_defer[o + task] = (uint32_t)best | (dsat << 16);
+                        p.decision_idx[o + task] = step;
+                        p.completion[o + task] = c_done;
+                        p.start_f1[o + task] = c_st0;
+                    }
+                    t_last = dev::dmax(t_last, c_done);
+                    step++;
+                    if (is_train) {
+                        j++;
+                        cur_defer = 0;
+                        a_tr = a_tr2;
+                        v_tr = v_tr2;
+                        if (j + 1 < nT) {
+                            a_tr2 = __ldg(p.arrival + o + nI + j + 1);
+                            v_tr2 = __ldg(p.lbk + o + nI + j + 1);
+                        }
+                        // next release: max(a_min, this task's S1 forward end)
+                        r = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
+                    } else {
+                        const double ttft = c_done - a;        // R from arrival
+                        sum_ttft = sum_ttft + ttft;
+                        double tauR;
+                        if (p.slo_mode == 1) {
+                            tauR = p.slo_const;
+                        } else {
+                            double acc = 0.0;
+                            for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * w;
+                            tauR = p.slo_mult * acc;
+                        }
+                        if (ttft <= tauR) n_slo++;          // SLO: TTFT <= 5x forward latency
+                        sum_ver += c_ver;
+                        a_last_inf = a;
+                        i++;
+                        a_inf = a_inf2;
+                        v_inf = v_inf2;
+                        if (i + 1 < nI) {
+                            a_inf2 = __ldg(p.arrival + o + i + 1);
+                            v_inf2 = __ldg(p.lbk + o + i + 1);
+                        }
+                    }
+                }
             }
         }
     }

@@ -14,7 +14,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liblemix.so")
+# LMX_LIB: developer override (A/B of alternative builds of the same sources)
+LIB_PATH = os.environ.get("LMX_LIB") or os.path.join(_HERE, "liblemix.so")
 
 LMX_OK, LMX_EINVAL, LMX_ESTATE, LMX_ENOMEM, LMX_ECUDA, LMX_ENCCL, LMX_EQCAP, LMX_EBUDGET = range(8)
 LMX_LEMIX, LMX_RR, LMX_SEPARATE, LMX_FIXED = range(4)
