@@ -40,10 +40,14 @@ static double MAX(double x, double y) { return (y > x) ? y : x; }
 static double MIN(double x, double y) { return (y < x) ? y : x; }
 
 /* ---------------------------------------------------------------------------
- * exp(-t), t >= 0: the fully specified routine of DESIGN.md [R-exp]
- * (Cody-Waite reduction by ln 2, degree-13 Taylor polynomial in Horner form,
- * multiply then add, no FMA; exact scaling by 2^k).  Pinned against libm in
- * tests/test_oracle_units.py (<= 2 ulp) and exact at t = 0.
+ * exp(-t), t >= 0: the fully specified routine of DESIGN.md [R-exp] (the
+ * paper only says "exp", Eq. 2; both sides must round identically):
+ *   k = rint(-t * log2(e)); r = (-t - k*LN2_HI) - k*LN2_LO
+ *   p = the degree-13 Taylor polynomial of e^r evaluated by Estrin's scheme
+ *       (pairs c_2i + c_2i+1*r, then powers r^2, r^4, r^8), each a*b+c as a
+ *       multiply then an add, no FMA
+ *   result = p * 2^k (exact; normal for t <= 700), 0 beyond t = 700.
+ * Pinned against libm in tests/test_oracle_units.py (<= 2 ulp), exact at 0.
  * ------------------------------------------------------------------------- */
 double orc_exp_neg(double t)
 {
@@ -51,15 +55,19 @@ double orc_exp_neg(double t)
         0x1p+0, 0x1p+0, 0x1p-1, 0x1.5555555555555p-3, 0x1.5555555555555p-5,
         0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
         0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
-        0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};
+        0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};   /* 1/i! */
     if (t > 700.0) return 0.0;
     double x = -t;
     double k = rint(x * 0x1.71547652b82fep0);       /* round half to even */
     double hi = x - k * 0x1.62e42fee00000p-1;      /* ln2 high part */
     double lo = k * 0x1.a39ef35793c76p-33;         /* ln2 low part */
     double r = hi - lo;
-    double p = C[13];
-    for (int i = 12; i >= 0; --i) p = p * r + C[i];
+    double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+    double q[7];
+    for (int i = 0; i < 7; ++i) q[i] = C[2 * i] + C[2 * i + 1] * r;   /* c_2i + c_2i+1 r */
+    double s0 = q[0] + q[1] * r2, s1 = q[2] + q[3] * r2, s2 = q[4] + q[5] * r2, s3 = q[6];
+    double u0 = s0 + s1 * r4, u1 = s2 + s3 * r4;
+    double p = u0 + u1 * r8;
     return ldexp(p, (int)k);
 }
 

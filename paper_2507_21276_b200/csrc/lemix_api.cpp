@@ -408,6 +408,10 @@ lmx_status lmx_run(lmx_ctx *c)
     k.S = c->S;
     int Tl = 1;
     while (Tl < c->N && Tl < 32) Tl <<= 1;
+    if (const char *tl_env = getenv("LMX_TILE_LANES")) {   // developer override: lanes per trace
+        const int want = atoi(tl_env);
+        if (want >= 1 && want <= 32 && (want & (want - 1)) == 0 && (c->N + want - 1) / want <= 4) Tl = want;
+    }
     k.T = Tl;
     k.log2T = 0;
     while ((1 << k.log2T) < Tl) k.log2T++;

@@ -28,19 +28,23 @@ namespace lmx {
 namespace {
 
 constexpr int kBlock = 128;                 // 4 warps per CTA
+#ifndef LMX_TILE_MINB
+#define LMX_TILE_MINB 3                     // resident CTAs/SM the register budget targets
+#endif
 using dev::kInf;
 using dev::kSqrt2Pi;
 using dev::task_batch;
 using dev::task_len;
 using dev::task_w;
 
-template <int SMAX, int NPL>
-__global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
+template <int SMAX, bool EXACT, int NPL>
+__global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t s_bar;
 
-    const int N = p.N, S = p.S, NS = p.N * p.S;
+    // S is a compile-time constant when it equals the template bucket (EXACT)
+    const int N = p.N, S = EXACT ? SMAX : p.S, NS = p.N * S;
     double *s_eta = reinterpret_cast<double *>(smem_raw);
 
     // ---- K1: stage eta_f | eta_b (16*N*S bytes) into shared memory via TMA ----
@@ -53,6 +57,9 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
     dev::mbar_wait(&s_bar, 0);
     const double *s_ef = s_eta;
     const double *s_eb = s_eta + NS;
+    double ef0[SMAX];   // eta_F of node 0, for tau_R (R-16)
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) ef0[s] = (s < S) ? s_ef[s] : 0.0;
 
     // ---- tile geometry ----
     const int lane = threadIdx.x & 31;
@@ -232,7 +239,9 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
                     tauR = p.slo_const;
                 } else {
                     double acc = 0.0;
-                    for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * wn;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s)
+                        if (s < S) acc = acc + ef0[s] * wn;
                     tauR = p.slo_mult * acc;
                 }
                 deferred = (m - t_inf) > tauR;
@@ -399,7 +408,6 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
                                 c_ver = ntr[jj] - (tail - k);
                             }
                             if (c_status == LMX_OK) {
-                                dev::advance_skip<SMAX>(sk[jj], P[jj], S, q, qh[jj], qh[jj] + qn[jj]);
                                 cnt[jj]++;
                                 sl[jj] += l;
                                 sl2[jj] += (long long)l * l;
@@ -452,7 +460,9 @@ __global__ void __launch_bounds__(kBlock) event_loop_kernel(const KParams p)
                             tauR = p.slo_const;
                         } else {
                             double acc = 0.0;
-                            for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * w;
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) acc = acc + ef0[s] * w;
                             tauR = p.slo_mult * acc;
                         }
                         if (ttft <= tauR) n_slo++;          // SLO: TTFT <= 5x forward latency
@@ -522,24 +532,30 @@ __global__ void __launch_bounds__(kCellBlock) cells_kernel(const CellParams c)
 
 typedef void (*kernel_fn)(const KParams);
 
-template <int SMAX>
+template <int SMAX, bool EXACT>
 kernel_fn pick_npl(int npl)
 {
     switch (npl) {
-    case 1: return event_loop_kernel<SMAX, 1>;
-    case 2: return event_loop_kernel<SMAX, 2>;
-    default: return event_loop_kernel<SMAX, 4>;
+    case 1: return event_loop_kernel<SMAX, EXACT, 1>;
+    case 2: return event_loop_kernel<SMAX, EXACT, 2>;
+    default: return event_loop_kernel<SMAX, EXACT, 4>;
     }
+}
+
+template <int SMAX>
+kernel_fn pick_exact(const KParams &p)
+{
+    return p.S == SMAX ? pick_npl<SMAX, true>(npl_bucket(p.npl)) : pick_npl<SMAX, false>(npl_bucket(p.npl));
 }
 
 kernel_fn pick(const KParams &p)
 {
     switch (max_stages_bucket(p.S)) {
-    case 1: return pick_npl<1>(npl_bucket(p.npl));
-    case 2: return pick_npl<2>(npl_bucket(p.npl));
-    case 4: return pick_npl<4>(npl_bucket(p.npl));
-    case 8: return pick_npl<8>(npl_bucket(p.npl));
-    default: return pick_npl<16>(npl_bucket(p.npl));
+    case 1: return pick_exact<1>(p);
+    case 2: return pick_exact<2>(p);
+    case 4: return pick_exact<4>(p);
+    case 8: return pick_exact<8>(p);
+    default: return pick_exact<16>(p);
     }
 }
 

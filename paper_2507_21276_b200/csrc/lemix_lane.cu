@@ -55,13 +55,14 @@ struct LaneSmem {
     static constexpr int kBytesPerThread = 8 * (kDoubles + kLongs) + 4 * kInts;
 };
 
-template <int NMAX, int SMAX>
+template <int NMAX, int SMAX, bool EXACT>
 __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(const KParams p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t s_bar;
 
-    const int N = p.N, S = p.S, NS = p.N * p.S;
+    // S is a compile-time constant when it equals the template bucket (EXACT)
+    const int N = p.N, S = EXACT ? SMAX : p.S, NS = p.N * S;
     double *s_eta = reinterpret_cast<double *>(smem_raw);
     if (threadIdx.x == 0) {
         dev::mbar_init(&s_bar, 1);
@@ -72,6 +73,9 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
     dev::mbar_wait(&s_bar, 0);
     const double *s_ef = s_eta;
     const double *s_eb = s_eta + NS;
+    double ef0[SMAX];   // eta_F of node 0, for tau_R (R-16)
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) ef0[s] = (s < S) ? s_ef[s] : 0.0;
 
     const int B = blockDim.x, tid = threadIdx.x;
     double *c_LB = s_eta + 2 * NS;                        // [SMAX][NMAX][B]
@@ -182,7 +186,9 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     tauR = p.slo_const;
                 } else {
                     double acc = 0.0;
-                    for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * wn;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s)
+                        if (s < S) acc = acc + ef0[s] * wn;
                     tauR = p.slo_mult * acc;
                 }
                 deferred = (m - t_inf) > tauR;
@@ -235,6 +241,9 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             const dev::Ring q{ring_be + (rb0 + n * K) * S, ring_w + rb0 + n * K, p.kmask, S};
                             dev::plan<SMAX>(P[n], (hasp >> n) & 1u, S, s_ef + n * S, s_eb + n * S, q, qh[n], qn[n],
                                             sk, w, a, now, en[n], st0[n], II, gc);
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) SK_(n, s) = sk[s];
                             qh[n] += gc;
                             qn[n] -= gc;
                             const double R = dev::last_of(en[n], S) - a;                         // line 20
@@ -299,6 +308,9 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     dev::plan<SMAX>(Pc, (hasp >> best) & 1u, S, s_ef + best * S, s_eb + best * S, q, qhc, qnc, sk,
                                     w, a, now, en_b, st0_b, II, gc);
 #pragma unroll
+                    for (int s = 0; s < SMAX; ++s)
+                        if (s < S) SK_(best, s) = sk[s];
+#pragma unroll
                     for (int n = 0; n < NMAX; ++n)
                         if (n == best) { qh[n] += gc; qn[n] -= gc; }
                 }
@@ -356,15 +368,6 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     ver = NTR_(best) - (qhb + qnb - k);
                 }
                 if (status == LMX_OK) {
-                    {   // stale-prefix pointers for the node's new P (see dev::plan)
-                        int sk[SMAX];
-#pragma unroll
-                        for (int s = 0; s < SMAX; ++s) sk[s] = SK_(best, s);
-                        dev::advance_skip<SMAX>(sk, en_b, S, qb, qhb, qhb + qnb);
-#pragma unroll
-                        for (int s = 0; s < SMAX; ++s)
-                            if (s < S) SK_(best, s) = sk[s];
-                    }
                     {   // P, a_[-1], Eq. 2 history of the chosen node
                         const int c = CNT_(best) + 1;
                         const long long s1 = SL_(best) + l, s2 = SL2_(best) + (long long)l * l;
@@ -417,7 +420,9 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             tauR = p.slo_const;
                         } else {
                             double acc = 0.0;
-                            for (int s = 0; s < S; ++s) acc = acc + s_ef[s] * w;
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) acc = acc + ef0[s] * w;
                             tauR = p.slo_mult * acc;
                         }
                         if (ttft <= tauR) n_slo++;
@@ -494,18 +499,24 @@ typedef void (*kernel_fn)(const KParams);
 int nodes_bucket(int N) { return N <= 2 ? 2 : N <= 4 ? 4 : 8; }
 int stages_bucket(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : 4; }
 
+template <int NMAX, int SMAX>
+kernel_fn pick_exact(int S)
+{
+    return S == SMAX ? lane_loop_kernel<NMAX, SMAX, true> : lane_loop_kernel<NMAX, SMAX, false>;
+}
+
 kernel_fn pick(int N, int S)
 {
     if (N < 1 || N > 8 || S < 1 || S > 4) return nullptr;
     switch (nodes_bucket(N) * 10 + stages_bucket(S)) {
-    case 21: return lane_loop_kernel<2, 1>;
-    case 22: return lane_loop_kernel<2, 2>;
-    case 24: return lane_loop_kernel<2, 4>;
-    case 41: return lane_loop_kernel<4, 1>;
-    case 42: return lane_loop_kernel<4, 2>;
-    case 44: return lane_loop_kernel<4, 4>;
-    case 81: return lane_loop_kernel<8, 1>;
-    case 82: return lane_loop_kernel<8, 2>;
+    case 21: return pick_exact<2, 1>(S);
+    case 22: return pick_exact<2, 2>(S);
+    case 24: return pick_exact<2, 4>(S);
+    case 41: return pick_exact<4, 1>(S);
+    case 42: return pick_exact<4, 2>(S);
+    case 44: return pick_exact<4, 4>(S);
+    case 81: return pick_exact<8, 1>(S);
+    case 82: return pick_exact<8, 2>(S);
     default: return nullptr;
     }
 }
