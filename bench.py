@@ -249,7 +249,10 @@ def main():
     tr = workload.mc_traces(T, seed_base=args.seed + rank * T, n_inf=args.n_inf, n_train=args.n_train,
                             out=(arrival_h.numpy(), lbk_h.numpy().view(np.uint32)), with_out_len=False)
     t_gen = time.perf_counter() - t_gen
-    stream = torch.cuda.current_stream()
+    # a dedicated stream: the library launches on it and the CUDA events below
+    # are recorded on it
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     arrival_d = arrival_h.to("cuda", non_blocking=True)
     lbk_d = lbk_h.to("cuda", non_blocking=True)
     torch.cuda.synchronize()
@@ -342,7 +345,8 @@ def main():
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": decisions_per_step / (float(te.item()) / args.steps), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "path": "lmx_load_traces(HOST, pinned) -> lmx_run -> lmx_sync -> lmx_get_cells"}
+               "path": ("lmx_load_traces(HOST, pinned) -> lmx_run (streams the inputs in 2^22-task chunks "
+                        "overlapped with the kernel) -> lmx_sync -> lmx_get_cells")}
 
     # ---------------- oracle: sampled parity + cpu_baseline + op counts ----------------
     cpu = None

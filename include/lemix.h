@@ -154,10 +154,13 @@ const char *lmx_last_error(const lmx_ctx *ctx);
 
 lmx_status lmx_load_profile(lmx_ctx *ctx, const lmx_profile *profile);
 
-/* HOST: task arrays are copied to device buffers owned by the context
- * (asynchronously on the context stream when the host memory is pinned).
+/* HOST: the task arrays are host memory (pinned for full overlap) borrowed
+ * until the next lmx_sync; lmx_run streams them into device buffers owned by
+ * the context on a second stream, in 2^22-task chunks, while the kernel
+ * already consumes the chunks that have landed (later runs reuse the copy).
  * DEVICE: the task arrays are borrowed device pointers and must stay valid
- * until the next lmx_sync.  offsets and n_inf are always host memory. */
+ * until the next lmx_sync.  offsets and n_inf are always host memory and are
+ * copied. */
 lmx_status lmx_load_traces(lmx_ctx *ctx, const lmx_traces *traces, lmx_mem mem);
 
 lmx_status lmx_set_params(lmx_ctx *ctx, const lmx_params *params);

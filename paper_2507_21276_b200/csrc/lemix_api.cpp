@@ -128,6 +128,16 @@ struct lmx_ctx {
     // traces
     bool have_traces = false;
     int64_t n_traces = 0, n_tasks = 0;
+    // host task arrays borrowed until the next lmx_sync; lmx_run streams them
+    // into HBM on copy_stream while the kernel runs (chunked, see wait_inputs)
+    const double *h_arrival = nullptr;
+    const uint32_t *h_lbk = nullptr;
+    bool host_pending = false;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_armed = nullptr, ev_copied = nullptr;
+    DevBuf ready;
+    unsigned *h_seq = nullptr;      // pinned 1..n: the values written to *ready
+    int64_t h_seq_len = 0;
     std::vector<int64_t> h_offsets;
     std::vector<int32_t> h_n_inf;
     bool has_fixed = false;
@@ -145,7 +155,7 @@ struct lmx_ctx {
     // outputs / state
     int per_task = 1;
     DevBuf node_defer, decision_idx, completion, start_f1;
-    DevBuf summaries, trace_err, work, first_bad, ring_be, ring_w;
+    DevBuf summaries, trace_err, work, first_bad, ring_be;
     bool ran = false, synced = false;
 
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -217,6 +227,10 @@ lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
     cudaEventCreate(&c->ev0);
     cudaEventCreate(&c->ev1);
     cudaEventCreate(&c->ev2);
+    cudaEventCreateWithFlags(&c->ev_armed, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_copied, cudaEventDisableTiming);
+    // non-blocking: must never be serialised behind the kernel it feeds
+    cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking);
     lmx_params_default(&c->par);
     if (c->work.ensure(8) != cudaSuccess || c->first_bad.ensure(8) != cudaSuccess) {
         g_create_error = "lmx_create: device allocation failed";
@@ -232,6 +246,13 @@ void lmx_destroy(lmx_ctx *c)
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->copy_stream) {
+        cudaStreamSynchronize(c->copy_stream);
+        cudaStreamDestroy(c->copy_stream);
+    }
+    if (c->ev_armed) cudaEventDestroy(c->ev_armed);
+    if (c->ev_copied) cudaEventDestroy(c->ev_copied);
+    if (c->h_seq) cudaFreeHost(c->h_seq);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
     if (c->ev2) cudaEventDestroy(c->ev2);
@@ -316,19 +337,18 @@ lmx_status lmx_load_traces(lmx_ctx *c, const lmx_traces *tr, lmx_mem mem)
             c->lbk.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess ||
             (c->has_fixed && c->fixed.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess))
             return c->fail(LMX_ENOMEM, "trace buffers allocation (" + std::to_string(M) + " tasks)");
-        if (M > 0) {
-            s = c->cuda(cudaMemcpyAsync(c->arrival.p, tr->arrival, M * 8, cudaMemcpyHostToDevice, c->stream),
-                        "arrival copy");
-            if (s == LMX_OK)
-                s = c->cuda(cudaMemcpyAsync(c->lbk.p, tr->len_batch_kind, M * 4, cudaMemcpyHostToDevice, c->stream),
-                            "len_batch_kind copy");
-            if (s == LMX_OK && c->has_fixed)
-                s = c->cuda(cudaMemcpyAsync(c->fixed.p, tr->fixed_node, M * 4, cudaMemcpyHostToDevice, c->stream),
-                            "fixed_node copy");
+        if (M > 0 && c->has_fixed) {
+            s = c->cuda(cudaMemcpyAsync(c->fixed.p, tr->fixed_node, M * 4, cudaMemcpyHostToDevice, c->stream),
+                        "fixed_node copy");
             if (s != LMX_OK) return s;
         }
+        // arrival / len_batch_kind are streamed by lmx_run, overlapped with the kernel
+        c->h_arrival = tr->arrival;
+        c->h_lbk = tr->len_batch_kind;
+        c->host_pending = M > 0;
         (void)is_pinned;
     }
+    if (mem == LMX_DEVICE) c->host_pending = false;
     c->n_traces = T;
     c->n_tasks = M;
     c->have_traces = true;
@@ -483,8 +503,7 @@ lmx_status lmx_run(lmx_ctx *c)
 
     // device buffers
     const size_t ring_entries = (size_t)tiles * k.npad * K;
-    if (c->ring_be.ensure(ring_entries * c->S * sizeof(double2)) != cudaSuccess ||
-        c->ring_w.ensure(ring_entries * sizeof(double)) != cudaSuccess)
+    if (c->ring_be.ensure(ring_entries * (c->S + 1) * sizeof(double2)) != cudaSuccess)
         return c->fail(LMX_ENOMEM, "queue ring allocation (" + std::to_string(ring_entries) + " entries; lower qcap)");
     if (c->summaries.ensure(std::max<int64_t>(T, 1) * sizeof(lmx_summary)) != cudaSuccess ||
         c->trace_err.ensure(std::max<int64_t>(T, 1) * 8) != cudaSuccess ||
@@ -507,11 +526,34 @@ lmx_status lmx_run(lmx_ctx *c)
     k.work = (unsigned long long *)c->work.p;
     k.first_bad = (unsigned long long *)c->first_bad.p;
     k.ring_be = (double2 *)c->ring_be.p;
-    k.ring_w = (double *)c->ring_w.p;
 
     lmx_status s = c->cuda(cudaMemsetAsync(c->work.p, 0, 8, c->stream), "reset");
     if (s == LMX_OK) s = c->cuda(cudaMemsetAsync(c->first_bad.p, 0xFF, 8, c->stream), "reset");
     if (s != LMX_OK) return s;
+
+    // streamed inputs: 2^22-task chunks (a multiple of 32 tasks, so chunk
+    // boundaries are 128-byte aligned in both arrays and no cache line mixes
+    // landed and in-flight data)
+    const bool stream_in = c->host_pending;
+    const int64_t chunk = int64_t(1) << 22;
+    const int64_t n_chunks = stream_in ? (M + chunk - 1) / chunk : 0;
+    if (stream_in) {
+        if (c->ready.ensure(4) != cudaSuccess) return c->fail(LMX_ENOMEM, "ready flag");
+        if (c->h_seq_len < n_chunks) {
+            if (c->h_seq) cudaFreeHost(c->h_seq);
+            c->h_seq = nullptr;
+            c->h_seq_len = 0;
+            if (cudaMallocHost(&c->h_seq, n_chunks * sizeof(unsigned)) != cudaSuccess)
+                return c->fail(LMX_ENOMEM, "pinned chunk sequence");
+            for (int64_t q = 0; q < n_chunks; ++q) c->h_seq[q] = (unsigned)(q + 1);
+            c->h_seq_len = n_chunks;
+        }
+        s = c->cuda(cudaMemsetAsync(c->ready.p, 0, 4, c->stream), "ready reset");
+        if (s != LMX_OK) return s;
+        cudaEventRecord(c->ev_armed, c->stream);
+        k.ready = (const unsigned *)c->ready.p;
+        k.chunk_tasks = chunk;
+    }
     c->launches = 0;
     cudaEventRecord(c->ev0, c->stream);
     if (T > 0) {
@@ -521,6 +563,26 @@ lmx_status lmx_run(lmx_ctx *c)
         c->launches++;
     }
     cudaEventRecord(c->ev1, c->stream);
+    if (stream_in) {
+        // the copies run on a non-blocking stream while the kernel consumes
+        // the chunks that have landed; the context stream then waits for them
+        cudaStreamWaitEvent(c->copy_stream, c->ev_armed, 0);
+        for (int64_t q = 0; q < n_chunks && s == LMX_OK; ++q) {
+            const int64_t b = q * chunk, e = std::min(M, b + chunk);
+            s = c->cuda(cudaMemcpyAsync((double *)c->arrival.p + b, c->h_arrival + b, (e - b) * 8,
+                                        cudaMemcpyHostToDevice, c->copy_stream), "arrival copy");
+            if (s == LMX_OK)
+                s = c->cuda(cudaMemcpyAsync((uint32_t *)c->lbk.p + b, c->h_lbk + b, (e - b) * 4,
+                                            cudaMemcpyHostToDevice, c->copy_stream), "len_batch_kind copy");
+            if (s == LMX_OK)
+                s = c->cuda(cudaMemcpyAsync(c->ready.p, c->h_seq + q, 4, cudaMemcpyHostToDevice, c->copy_stream),
+                            "ready flag");
+        }
+        cudaEventRecord(c->ev_copied, c->copy_stream);
+        cudaStreamWaitEvent(c->stream, c->ev_copied, 0);
+        if (s != LMX_OK) return s;
+        c->host_pending = false;   // the data now lives in the context's buffers
+    }
 
     lmx::CellParams cp{};
     cp.n_traces = T;

@@ -27,6 +27,10 @@ struct KParams {
     const uint32_t *lbk;       // device [n_tasks]
     const int32_t *fixed;      // device [n_tasks] or nullptr
     const double *eta;         // device [2*N*S]: eta_f then eta_b, node-major
+    // streamed inputs (lmx_run with host traces): chunks of chunk_tasks tasks
+    // land in order; *ready = number of chunks copied (nullptr: all resident)
+    const unsigned *ready;
+    long long chunk_tasks;
 
     uint32_t *node_defer;      // outputs, nullptr = summary-only
     int32_t *decision_idx;
@@ -38,8 +42,7 @@ struct KParams {
     unsigned long long *work;  // device [1]: next trace to claim
     unsigned long long *first_bad;  // device [1]: min failing trace index
 
-    double2 *ring_be;          // [tile_slots][Npad][K][S] (start_b, end_b)
-    double *ring_w;            // [tile_slots][Npad][K]    C*l^2 of the entry
+    double2 *ring_be;          // [tile_slots][Npad][K][S+1]: (start_b, end_b) per stage, (C*l^2, 0)
     int32_t npad;              // npl * T
 };
 

@@ -28,6 +28,9 @@ namespace lmx {
 namespace {
 
 constexpr int kBlock = 128;                 // 4 warps per CTA
+#ifndef LMX_TILE_PF
+#define LMX_TILE_PF false                   // up-front ring loads in Alg. 1 (see dev::plan)
+#endif
 #ifndef LMX_TILE_MINB
 #define LMX_TILE_MINB 3                     // resident CTAs/SM the register budget targets
 #endif
@@ -72,12 +75,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
 
     // the Q_train ring of each node this lane owns
     double2 *rbe[NPL];
-    double *rwv[NPL];
 #pragma unroll
     for (int jj = 0; jj < NPL; ++jj) {
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
-        rbe[jj] = p.ring_be + rbase * S;
-        rwv[jj] = p.ring_w + rbase;
+        rbe[jj] = p.ring_be + rbase * (S + 1);
     }
 
     // ---- per-trace (tile-replicated) state ----
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 t = (long long)tt;
                 o = p.offsets[t];
                 const int len = (int)(p.offsets[t + 1] - o);
+                dev::wait_inputs(p.ready, p.chunk_tasks, o, o + len);
                 nI = p.n_inf[t];
                 nT = len - nI;
                 i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
@@ -309,8 +311,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         double II;
                         int gc;
                         const int qhead = qh[jj], qlen = qn[jj];
-                        const dev::Ring q{rbe[jj], rwv[jj], p.kmask, S};
-                        dev::plan<SMAX>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
+                        const dev::Ring q{rbe[jj], p.kmask, S};
+                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
                                         a, now, en_s[jj], st0_s[jj], II, gc);
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
                         // end_b^1 is non-decreasing along the queue)
@@ -362,7 +364,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         if (jj == jb) {
                             const double *ef = s_ef + best * S;
                             const double *eb = s_eb + best * S;
-                            const dev::Ring q{rbe[jj], rwv[jj], p.kmask, S};
+                            const dev::Ring q{rbe[jj], p.kmask, S};
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
                                 if (s < S) {
@@ -386,11 +388,11 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                                         const double sb = dev::dmax(x, LB[jj][s]);
                                         const double ebv = sb + eb[s] * w;
                                         LB[jj][s] = ebv;
-                                        rbe[jj][slot * S + s] = make_double2(sb, ebv);
+                                        rbe[jj][slot * (S + 1) + s] = make_double2(sb, ebv);
                                         x = ebv;
                                     }
                                 }
-                                rwv[jj][slot] = w;
+                                rbe[jj][slot * (S + 1) + S] = make_double2(w, 0.0);
                                 qn[jj]++;
 #pragma unroll
                                 for (int s = 0; s < SMAX; ++s)

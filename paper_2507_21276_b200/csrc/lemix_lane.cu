@@ -33,6 +33,9 @@ namespace lmx {
 namespace {
 
 constexpr int kLaneBlock = 128;
+#ifndef LMX_LANE_PF
+#define LMX_LANE_PF true                    // up-front ring loads in Alg. 1 (see dev::plan)
+#endif
 #ifndef LMX_LANE_MINB
 #define LMX_LANE_MINB 4   // resident CTAs/SM the register budget targets
 #endif
@@ -107,7 +110,6 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
     const long long K = (long long)p.kmask + 1;
     const long long rb0 = gthread * NMAX * K;               // ring of node n: rb0 + n*K
     const double2 *__restrict__ ring_be = p.ring_be;
-    const double *__restrict__ ring_w = p.ring_w;
 
     // ---- hot per-node state (registers) ----
     double P[NMAX][SMAX];
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
         const long long o = p.offsets[t];
         const int nI = p.n_inf[t];
         const int nT = (int)(p.offsets[t + 1] - o) - nI;
+        dev::wait_inputs(p.ready, p.chunk_tasks, o, o + nI + nT);
 
         int i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0, cur_defer = 0;
         int status = LMX_OK, err_task = 0, err_code = kErrNone;
@@ -238,8 +241,8 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             for (int s = 0; s < SMAX; ++s) sk[s] = SK_(n, s);
                             double II;
                             int gc;
-                            const dev::Ring q{ring_be + (rb0 + n * K) * S, ring_w + rb0 + n * K, p.kmask, S};
-                            dev::plan<SMAX>(P[n], (hasp >> n) & 1u, S, s_ef + n * S, s_eb + n * S, q, qh[n], qn[n],
+                            const dev::Ring q{ring_be + (rb0 + n * K) * (S + 1), p.kmask, S};
+                            dev::plan<SMAX, LMX_LANE_PF>(P[n], (hasp >> n) & 1u, S, s_ef + n * S, s_eb + n * S, q, qh[n], qn[n],
                                             sk, w, a, now, en[n], st0[n], II, gc);
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
@@ -304,8 +307,8 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     for (int s = 0; s < SMAX; ++s) sk[s] = SK_(best, s);
                     double II;
                     int gc;
-                    const dev::Ring q{ring_be + (rb0 + best * K) * S, ring_w + rb0 + best * K, p.kmask, S};
-                    dev::plan<SMAX>(Pc, (hasp >> best) & 1u, S, s_ef + best * S, s_eb + best * S, q, qhc, qnc, sk,
+                    const dev::Ring q{ring_be + (rb0 + best * K) * (S + 1), p.kmask, S};
+                    dev::plan<SMAX, LMX_LANE_PF>(Pc, (hasp >> best) & 1u, S, s_ef + best * S, s_eb + best * S, q, qhc, qnc, sk,
                                     w, a, now, en_b, st0_b, II, gc);
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s)
@@ -322,9 +325,8 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
 #pragma unroll
                 for (int n = 1; n < NMAX; ++n)
                     if (n == best) { qhb = qh[n]; qnb = qn[n]; }
-                double2 *rbe = p.ring_be + (rb0 + best * K) * S;
-                double *rwv = p.ring_w + rb0 + best * K;
-                const dev::Ring qb{rbe, rwv, p.kmask, S};
+                double2 *rbe = p.ring_be + (rb0 + best * K) * (S + 1);
+                const dev::Ring qb{rbe, p.kmask, S};
 #pragma unroll
                 for (int s = 0; s < SMAX; ++s)
                     if (s < S) BUSY_(best, s) = BUSY_(best, s) + ef[s] * w;
@@ -342,11 +344,11 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             const double sb = dmax(x, LB_(best, s));
                             const double ebv = sb + eb[s] * w;
                             LB_(best, s) = ebv;
-                            rbe[slot * S + s] = make_double2(sb, ebv);
+                            rbe[slot * (S + 1) + s] = make_double2(sb, ebv);
                             x = ebv;
                         }
                     }
-                    rwv[slot] = w;
+                    rbe[slot * (S + 1) + S] = make_double2(w, 0.0);
                     qnb++;
 #pragma unroll
                     for (int n = 0; n < NMAX; ++n)
