@@ -1,0 +1,550 @@
+// lemix_tile.cuh -- the tile-of-lanes persistent event-loop kernel template
+// (included by lemix_tile_lemix.cu and lemix_tile_base.cu, one translation
+// unit per policy class so the instantiations compile in parallel).
+//
+// K1 profile staging : the fp64 SoA profile table (eta_f, eta_b) is copied
+//                      into shared memory once per CTA with a TMA bulk copy
+//                      (cp.async.bulk + mbarrier).
+// K2-K4 event loop   : one persistent kernel.  A "tile" of T lanes of a warp
+//                      owns one trace at a time; lane l plans nodes l, l+T, ...
+//                      (Algorithm 1) and scores them (Eq. 1-3,
+//                      PAPER.md:546-565); a tile shuffle takes the arg-best with
+//                      the lowest-index tie-break; the owning
+//                      lane commits.  Eq. 4 is a tile min.
+//                      Tiles claim traces from a global counter until none are
+//                      left, so long and short traces balance across SMs.
+//
+// Compiled with --fmad=false: see lemix_device.cuh for the fp64 discipline.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+
+#include "lemix_device.cuh"
+#include "lemix_internal.h"
+
+#ifndef LMX_TILE_PF
+#define LMX_TILE_PF false                   // up-front ring loads in Alg. 1 (see dev::plan)
+#endif
+#ifndef LMX_TILE_WIN
+#define LMX_TILE_WIN 8                      // ring tail-window entries in shared memory (S <= 2)
+#endif
+#ifndef LMX_TILE_MINB
+#define LMX_TILE_MINB 3                     // resident CTAs/SM the register budget targets
+#endif
+
+namespace lmx {
+namespace tile {
+
+constexpr int kBlock = 128;                 // 4 warps per CTA
+using dev::kInf;
+using dev::kSqrt2Pi;
+using dev::task_batch;
+using dev::task_len;
+using dev::task_w;
+
+inline int stages_bucket(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16; }
+inline int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
+inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN : 0; }
+
+template <int SMAX, bool EXACT, int NPL, bool LEMIX>
+__global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
+{
+    // LEMIX: the policy is LeMix (all candidates planned and scored); else one
+    // of the baselines (RR / Separate / Fixed) picks the node first.
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ __align__(8) uint64_t s_bar;
+
+    // S is a compile-time constant when it equals the template bucket (EXACT)
+    const int N = p.N, S = EXACT ? SMAX : p.S, NS = p.N * S;
+    double *s_eta = reinterpret_cast<double *>(smem_raw);
+
+    // ---- K1: stage eta_f | eta_b (16*N*S bytes) into shared memory via TMA ----
+    if (threadIdx.x == 0) {
+        dev::mbar_init(&s_bar, 1);
+        dev::mbar_arrive_expect_tx(&s_bar, 16u * (uint32_t)NS);
+        dev::bulk_copy_g2s(s_eta, p.eta, 16u * (uint32_t)NS, &s_bar);
+    }
+    __syncthreads();
+    dev::mbar_wait(&s_bar, 0);
+    const double *s_ef = s_eta;
+    const double *s_eb = s_eta + NS;
+    double ef0[SMAX];   // eta_F of node 0, for tau_R (R-16)
+#pragma unroll
+    for (int s = 0; s < SMAX; ++s) ef0[s] = (s < S) ? s_ef[s] : 0.0;
+
+    // ---- tile geometry ----
+    const int lane = threadIdx.x & 31;
+    const int T = p.T, log2T = p.log2T;
+    const int tl = lane & (T - 1);
+    const int tbase = lane & ~(T - 1);
+    const unsigned tmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << tbase);
+    const long long gtile = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> log2T;
+    const long long K = (long long)p.kmask + 1;
+
+    // the Q_train ring of each node this lane owns
+    // ring tail window (shared memory), [slot jj][W][S+1][thread]
+    constexpr int W = (SMAX <= 2) ? LMX_TILE_WIN : 0;   // see window_entries()
+    double2 *win[NPL];
+#pragma unroll
+    for (int jj = 0; jj < NPL; ++jj)
+        win[jj] = reinterpret_cast<double2 *>(smem_raw + 16 * NS) + (jj * (W > 0 ? W : 1) * (S + 1)) * blockDim.x +
+                  threadIdx.x;
+    double2 *rbe[NPL];
+#pragma unroll
+    for (int jj = 0; jj < NPL; ++jj) {
+        const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
+        rbe[jj] = p.ring_be + rbase * (S + 1);
+    }
+
+    // ---- per-trace (tile-replicated) state ----
+    bool active = false, finished = false;
+    long long t = 0, o = 0;
+    const double *tarr = p.arrival;      // this trace's task arrays (32-bit indexing)
+    const uint32_t *tlbk = p.lbk;
+    int nI = 0, nT = 0, i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0;
+    int cur_defer = 0, status = LMX_OK, err_task = 0, err_code = kErrNone;
+    double r = kInf, t_first = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
+    long long n_slo = 0, sum_ver = 0, n_def = 0;
+    double a_inf = 0.0, a_inf2 = 0.0, a_tr = 0.0, a_tr2 = 0.0;   // 2-deep input prefetch
+    uint32_t v_inf = 0, v_inf2 = 0, v_tr = 0, v_tr2 = 0;
+
+    // ---- per-node state of this lane's slots (registers) ----
+    double P[NPL][SMAX], LB[NPL][SMAX], busy[NPL][SMAX];
+    double aprev[NPL], mu[NPL], kk[NPL], cc[NPL];
+    int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL], ntr[NPL], vp[NPL];
+    int sk[NPL][SMAX];   // stale-prefix pointers (see dev::plan)
+    long long sl[NPL], sl2[NPL];
+
+    // Control flow inside the loop is structured (no continue/break out of a
+    // branch) so tiles that took different branches reconverge right after it.
+    while (!__all_sync(0xffffffffu, finished)) {
+        if (!finished && !active) {
+            // ---- claim the next trace ----
+            unsigned long long tt = 0;
+            if (tl == 0) tt = atomicAdd(p.work, 1ull);
+            tt = __shfl_sync(tmask, tt, tbase);
+            if (tt >= (unsigned long long)p.n_traces) {
+                finished = true;
+            } else {
+                t = (long long)tt;
+                o = p.offsets[t];
+                const int len = (int)(p.offsets[t + 1] - o);
+                dev::wait_inputs(p.ready, p.chunk_tasks, o, o + len);
+                nI = p.n_inf[t];
+                nT = len - nI;
+                tarr = p.arrival + o;
+                tlbk = p.lbk + o;
+                i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
+                status = LMX_OK;
+                err_task = 0;
+                err_code = kErrNone;
+                n_slo = sum_ver = n_def = 0;
+                sum_ttft = 0.0;
+                t_last = -kInf;
+                a_last_inf = -kInf;
+                if (nI > 0) { a_inf = __ldg(tarr); v_inf = __ldg(tlbk); }
+                if (nI > 1) { a_inf2 = __ldg(tarr + 1); v_inf2 = __ldg(tlbk + 1); }
+                if (nT > 0) { a_tr = __ldg(tarr + nI); v_tr = __ldg(tlbk + nI); }
+                if (nT > 1) { a_tr2 = __ldg(tarr + nI + 1); v_tr2 = __ldg(tlbk + nI + 1); }
+                r = (nT > 0) ? a_tr : kInf;
+                t_first = kInf;
+                if (nI > 0) t_first = dev::dmin(t_first, a_inf);
+                if (nT > 0) t_first = dev::dmin(t_first, a_tr);
+#pragma unroll
+                for (int jj = 0; jj < NPL; ++jj) {
+                    hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = ntr[jj] = vp[jj] = 0;
+                    sl[jj] = sl2[jj] = 0;
+                    aprev[jj] = mu[jj] = kk[jj] = cc[jj] = 0.0;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) {
+                        P[jj][s] = 0.0;
+                        LB[jj][s] = -kInf;
+                        busy[jj][s] = 0.0;
+                        sk[jj][s] = 0;
+                    }
+                }
+                if (!LEMIX && p.policy == LMX_SEPARATE && N == 1 && nI > 0 && nT > 0) {
+                    status = LMX_EINVAL;
+                    err_code = kErrSeparateN1;
+                }
+                active = true;
+            }
+        }
+        if (!active) continue;   // (finished lanes only: back to the warp vote)
+
+        if (status == LMX_OK && (i < nI || j < nT) && ++iters > 2 * (nI + nT) + 2) status = LMX_EBUDGET;
+        const bool done_trace = (status != LMX_OK) || (i >= nI && j >= nT);
+
+        if (done_trace) {
+            // ---- per-trace metrics, node folds in node order ----
+            lmx_summary sm;
+            sm.n_tasks = nI + nT;
+            sm.n_inf = nI;
+            sm.n_train = nT;
+            sm.status = status;
+            sm.n_slo_met = sm.n_deferrals = sm.active_nodes = sm.sum_version = 0;
+            sm.makespan = sm.throughput = sm.sum_ttft = sm.mean_ttft = sm.slo_attainment = 0.0;
+            sm.mean_util = sm.mean_len_std = 0.0;
+            if (status == LMX_OK) {
+                const int ntask = nI + nT;
+                sm.n_slo_met = n_slo;
+                sm.n_deferrals = n_def;
+                sm.sum_version = sum_ver;
+                sm.sum_ttft = sum_ttft;
+                sm.makespan = (ntask > 0) ? t_last - t_first : 0.0;
+                sm.throughput = (sm.makespan > 0.0) ? (double)ntask / sm.makespan : 0.0;
+                sm.mean_ttft = (nI > 0) ? sum_ttft / (double)nI : 0.0;
+                sm.slo_attainment = (nI > 0) ? (double)n_slo / (double)nI : 1.0;
+                double U = 0.0, stds = 0.0;
+                long long act = 0;
+                for (int n = 0; n < N; ++n) {
+                    const int src = tbase + (n & (T - 1));
+                    const int jn = n >> log2T;
+                    long long c = 0, v2 = 0;
+#pragma unroll
+                    for (int jj = 0; jj < NPL; ++jj)
+                        if (jj == jn) { c = cnt[jj]; v2 = (long long)cnt[jj] * sl2[jj] - sl[jj] * sl[jj]; }
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) {
+                        if (s < S) {
+                            double bv = 0.0;
+#pragma unroll
+                            for (int jj = 0; jj < NPL; ++jj)
+                                if (jj == jn) bv = busy[jj][s];
+                            U = U + dev::shfl_d(tmask, bv, src);
+                        }
+                    }
+                    double sd = (c > 0) ? sqrt((double)v2) / (double)c : 0.0;
+                    sd = dev::shfl_d(tmask, sd, src);
+                    c = __shfl_sync(tmask, c, src);
+                    if (c > 0) {
+                        act++;
+                        stds = stds + sd;
+                    }
+                }
+                sm.active_nodes = act;
+                sm.mean_util = (sm.makespan > 0.0) ? U / ((double)(N * S) * sm.makespan) : 0.0;
+                sm.mean_len_std = (act > 0) ? stds / (double)act : 0.0;
+            }
+            if (tl == 0) {
+                p.summaries[t] = sm;
+                if (status != LMX_OK) {
+                    p.trace_err[t] = ((long long)err_task << 8) | err_code;
+                    atomicMin(p.first_bad, (unsigned long long)t);
+                }
+            }
+            active = false;
+        } else {
+            // ---- a1: event selection (ties -> inference) ----
+            const double t_inf = (i < nI) ? a_inf : kInf;
+            const bool is_train = !(t_inf <= r);
+            const double now = is_train ? r : t_inf;
+            const uint32_t v = is_train ? v_tr : v_inf;
+            bool deferred = false;
+            if (LEMIX && is_train && p.deprioritize && i < nI) {
+                // ---- a2: Eq. 4 queue-level deprioritisation against the next
+                // enqueued inference task (R-14/R-15) ----
+                const double wn = task_w(v_inf);
+                double m = kInf;
+#pragma unroll
+                for (int jj = 0; jj < NPL; ++jj) {
+                    const int n = tl + jj * T;
+                    if (n < N) {
+                        const double latest = hasp[jj] ? dev::last_of(P[jj], S) : -kInf;
+                        m = dev::dmin(m, latest + s_ef[n * S + S - 1] * wn);
+                    }
+                }
+                for (int off = T >> 1; off > 0; off >>= 1) m = dev::dmin(m, dev::shfl_xor_d(tmask, m, off));
+                double tauR;
+                if (p.slo_mode == 1) {
+                    tauR = p.slo_const;
+                } else {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s)
+                        if (s < S) acc = acc + ef0[s] * wn;
+                    tauR = p.slo_mult * acc;
+                }
+                deferred = (m - t_inf) > tauR;
+                if (deferred) {
+                    r = t_inf;          // move behind the next inference task
+                    cur_defer++;
+                    n_def++;
+                }
+            }
+            const int task = is_train ? nI + j : i;
+            if (!deferred) {
+                // ---- input validation of the task being placed (one predicate;
+                // the error code is worked out only on the rare failure path) ----
+                const double arr = is_train ? a_tr : a_inf;
+                const unsigned lv = (unsigned)task_len(v);
+                bool ok = ((v >> 21) == 0u) & (lv - 1u < 2048u) & (task_batch(v) >= 1) &
+                          ((int)((v >> 20) & 1u) == (int)is_train) & (arr >= 0.0) & (arr < kInf) &
+                          (is_train | (arr >= a_last_inf));
+                int fx = 0;
+                if (!LEMIX && p.policy == LMX_FIXED) {
+                    fx = __ldg(p.fixed + o + task);
+                    ok = ok & (fx >= 0) & (fx < N);
+                }
+                if (!ok) {
+                    int code = kErrFixed;
+                    if (v >> 21) code = kErrBits;
+                    else if (task_len(v) < 1 || task_len(v) > 2048) code = kErrLen;
+                    else if (task_batch(v) < 1) code = kErrBatch;
+                    else if ((int)((v >> 20) & 1u) != (int)is_train) code = kErrKind;
+                    else if (!(arr >= 0.0 && arr < kInf)) code = kErrArrival;
+                    else if (!is_train && arr < a_last_inf) code = kErrOrder;
+                    status = LMX_EINVAL;
+                    err_task = task;
+                    err_code = code;
+                }
+            }
+            if (!deferred && status == LMX_OK) {
+                const double a = now;                    // dispatch time (R-2)
+                const double w = task_w(v);
+                const int l = task_len(v);
+
+                // ---- a9: baseline selectors ----
+                int chosen = -1;
+                if (LEMIX) {
+                } else if (p.policy == LMX_RR) {
+                    chosen = rr % N;
+                    rr++;
+                } else if (p.policy == LMX_SEPARATE) {
+                    if (!(nI > 0 && nT > 0)) {
+                        chosen = is_train ? (sep_t++ % N) : (sep_i++ % N);
+                    } else if (is_train) {
+                        chosen = (N - p.n_tr_sep) + (sep_t++ % p.n_tr_sep);
+                    } else {
+                        chosen = sep_i++ % (N - p.n_tr_sep);
+                    }
+                } else {
+                    chosen = __ldg(p.fixed + o + task);
+                }
+
+                // ---- a3-a7: Algorithm 1 + Eq. 1-3 for every candidate this lane owns ----
+                double en_s[NPL][SMAX];
+                double st0_s[NPL];
+                double f_best = 0.0;
+                int n_best = INT_MAX;
+#pragma unroll
+                for (int jj = 0; jj < NPL; ++jj) {
+                    const int n = tl + jj * T;
+                    st0_s[jj] = 0.0;
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) en_s[jj][s] = 0.0;
+                    if (n < N && (LEMIX || n == chosen)) {
+                        double II;
+                        int gc;
+                        const int qhead = qh[jj], qlen = qn[jj];
+                        const dev::RingT<W> q{rbe[jj], p.kmask, S, win[jj], (int)blockDim.x, qhead + qlen};
+                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
+                                        a, now, en_s[jj], st0_s[jj], II, gc);
+                        // lines 17-18: executed entries leave Q_train^n (a head advance:
+                        // end_b^1 is non-decreasing along the queue)
+                        qh[jj] = qhead + gc;
+                        qn[jj] = qlen - gc;
+                        if (LEMIX) {
+                            const double R = dev::last_of(en_s[jj], S) - a;               // line 20
+                            const double a_last = hasp[jj] ? aprev[jj] : a;               // R-9
+                            const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
+                            const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
+                            double LC;                                                    // Eq. 2
+                            if (cnt[jj] < 2) {
+                                LC = p.lc0;
+                            } else {
+                                const double d = (double)l - mu[jj];
+                                LC = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
+                            }
+                            const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
+                            if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
+                        }
+                    }
+                }
+
+                // ---- a8: arg-best over the tile: highest f, then lowest node index ----
+                int best;
+                if (LEMIX) {
+                    for (int off = T >> 1; off > 0; off >>= 1) {
+                        const double f2 = dev::shfl_xor_d(tmask, f_best, off);
+                        const int n2 = __shfl_xor_sync(tmask, n_best, off);
+                        if (n2 != INT_MAX &&
+                            (n_best == INT_MAX || f2 > f_best || (f2 == f_best && n2 < n_best))) {
+                            f_best = f2;
+                            n_best = n2;
+                        }
+                    }
+                    best = n_best;
+                } else {
+                    best = chosen;
+                }
+
+                // ---- a10: commit on the owning lane ----
+                const int owner = tbase + (best & (T - 1));
+                const int jb = best >> log2T;
+                double c_done = 0.0, c_en0 = 0.0, c_st0 = 0.0;
+                int c_ver = 0, c_status = LMX_OK;
+                if (lane == owner) {
+#pragma unroll
+                    for (int jj = 0; jj < NPL; ++jj) {
+                        if (jj == jb) {
+                            const double *ef = s_ef + best * S;
+                            const double *eb = s_eb + best * S;
+                            const dev::RingT<W> q{rbe[jj], p.kmask, S, win[jj], (int)blockDim.x, qh[jj] + qn[jj]};
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) {
+                                    P[jj][s] = en_s[jj][s];
+                                    busy[jj][s] = busy[jj][s] + ef[s] * w;
+                                }
+                            hasp[jj] = 1;
+                            aprev[jj] = a;
+                            c_en0 = en_s[jj][0];
+                            c_st0 = st0_s[jj];
+                            c_done = dev::last_of(en_s[jj], S);
+                            if (is_train && qn[jj] >= p.qcap) {
+                                c_status = LMX_EQCAP;
+                            } else if (is_train) {
+                                // backward planning, stages S..1
+                                const int slot = (qh[jj] + qn[jj]) & p.kmask;
+                                double x = c_done;
+#pragma unroll
+                                for (int s = SMAX - 1; s >= 0; --s) {
+                                    if (s < S) {
+                                        const double sb = dev::dmax(x, LB[jj][s]);
+                                        const double ebv = sb + eb[s] * w;
+                                        LB[jj][s] = ebv;
+                                        rbe[jj][slot * (S + 1) + s] = make_double2(sb, ebv);
+                                        if (W > 0)
+                                            win[jj][(((qh[jj] + qn[jj]) & (W - 1)) * (S + 1) + s) * blockDim.x] =
+                                                make_double2(sb, ebv);
+                                        x = ebv;
+                                    }
+                                }
+                                rbe[jj][slot * (S + 1) + S] = make_double2(w, 0.0);
+                                if (W > 0)
+                                    win[jj][(((qh[jj] + qn[jj]) & (W - 1)) * (S + 1) + S) * blockDim.x] =
+                                        make_double2(w, 0.0);
+                                qn[jj]++;
+#pragma unroll
+                                for (int s = 0; s < SMAX; ++s)
+                                    if (s < S) busy[jj][s] = busy[jj][s] + eb[s] * w;
+                                ntr[jj]++;
+                                c_done = x;
+                            } else {
+                                // version-at-inference: completed backwards form a prefix of
+                                // Q_train; start_f^1 of successive commits on a node is
+                                // non-decreasing, so the boundary pointer only moves forward.
+                                int k = vp[jj] > qh[jj] ? vp[jj] : qh[jj];
+                                const int tail = qh[jj] + qn[jj];
+                                while (k < tail && q.at(k, 0).y <= c_st0) k++;
+                                vp[jj] = k;
+                                c_ver = ntr[jj] - (tail - k);
+                            }
+                            if (c_status == LMX_OK) {
+                                cnt[jj]++;
+                                sl[jj] += l;
+                                sl2[jj] += (long long)l * l;
+                                if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (population mean / sigma)
+                                    const long long c = cnt[jj];
+                                    mu[jj] = (double)sl[jj] / (double)c;
+                                    const long long var = c * sl2[jj] - sl[jj] * sl[jj];
+                                    const double sigma = dev::dmax(sqrt((double)var) / (double)c, p.sigma_floor);
+                                    kk[jj] = 0.5 / (sigma * sigma);
+                                    cc[jj] = 1.0 / (sigma * kSqrt2Pi);
+                                }
+                            }
+                        }
+                    }
+                }
+                c_done = dev::shfl_d(tmask, c_done, owner);
+                c_en0 = dev::shfl_d(tmask, c_en0, owner);
+                c_st0 = dev::shfl_d(tmask, c_st0, owner);
+                c_ver = __shfl_sync(tmask, c_ver, owner);
+                c_status = __shfl_sync(tmask, c_status, owner);
+                if (c_status != LMX_OK) {
+                    status = c_status;
+                } else {
+                    // ---- a11: outputs + per-trace folds ----
+                    if (tl == 0 && p.node_defer) {
+                        const unsigned dsat = is_train ? (unsigned)min(cur_defer, 0xFFFF) : 0u;
+                        p.node_defer[o + task] = (uint32_t)best | (dsat << 16);
+                        p.decision_idx[o + task] = step;
+                        p.completion[o + task] = c_done;
+                        p.start_f1[o + task] = c_st0;
+                    }
+                    t_last = dev::dmax(t_last, c_done);
+                    step++;
+                    if (is_train) {
+                        j++;
+                        cur_defer = 0;
+                        a_tr = a_tr2;
+                        v_tr = v_tr2;
+                        {   // prefetch two ahead (clamped index: no branch)
+                            const int jn = min(j + 1, nT - 1);
+                            a_tr2 = __ldg(tarr + nI + jn);
+                            v_tr2 = __ldg(tlbk + nI + jn);
+                        }
+                        // next release: max(a_min, this task's S1 forward end)
+                        r = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
+                    } else {
+                        const double ttft = c_done - a;        // R from arrival
+                        sum_ttft = sum_ttft + ttft;
+                        double tauR;
+                        if (p.slo_mode == 1) {
+                            tauR = p.slo_const;
+                        } else {
+                            double acc = 0.0;
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) acc = acc + ef0[s] * w;
+                            tauR = p.slo_mult * acc;
+                        }
+                        if (ttft <= tauR) n_slo++;          // SLO: TTFT <= 5x forward latency
+                        sum_ver += c_ver;
+                        a_last_inf = a;
+                        i++;
+                        a_inf = a_inf2;
+                        v_inf = v_inf2;
+                        {   // prefetch two ahead (clamped index: no branch)
+                            const int in2 = min(i + 1, nI - 1);
+                            a_inf2 = __ldg(tarr + in2);
+                            v_inf2 = __ldg(tlbk + in2);
+                        }
+                    }
+                }
+            }
+        }
+    }
+}
+
+
+typedef void (*kernel_fn)(const KParams);
+
+template <int SMAX, bool EXACT, bool LEMIX>
+kernel_fn pick_npl(int npl)
+{
+    switch (npl) {
+    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX>;
+    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX>;
+    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX>;
+    }
+}
+
+template <bool LEMIX>
+kernel_fn pick(const KParams &p)
+{
+    const int nb = npl_bucket(p.npl);
+    switch (stages_bucket(p.S)) {
+    case 1: return pick_npl<1, true, LEMIX>(nb);
+    case 2: return p.S == 2 ? pick_npl<2, true, LEMIX>(nb) : pick_npl<2, false, LEMIX>(nb);
+    case 4: return p.S == 4 ? pick_npl<4, true, LEMIX>(nb) : pick_npl<4, false, LEMIX>(nb);
+    case 8: return p.S == 8 ? pick_npl<8, true, LEMIX>(nb) : pick_npl<8, false, LEMIX>(nb);
+    default: return p.S == 16 ? pick_npl<16, true, LEMIX>(nb) : pick_npl<16, false, LEMIX>(nb);
+    }
+}
+
+}  // namespace tile
+}  // namespace lmx
