@@ -204,17 +204,22 @@ static double idleness_profit(double II, int S, double a, double a_last, double 
 /* Eq. 2: LC = 1/(σ√(2π)) · exp{-(ℓ-μ)²/(2σ²)} with μ, σ the population mean
  * and standard deviation of lengths previously run on the node ([R-10]);
  * σ floored at sigma_floor, fewer than two samples -> lc0 ([R-11]).
+ * Arithmetic per DESIGN.md [R-stat]: one reciprocal of the count and one of σ
+ *   inv_c = 1/cnt; μ = Σℓ·inv_c; σ = max(√(cnt·Σℓ² − (Σℓ)²)·inv_c, floor);
+ *   inv_σ = 1/σ; k = (0.5·inv_σ)·inv_σ = 1/(2σ²); c = inv_σ·(1/√(2π)).
  * parity unpinned for lc0 (a reading, not a formula). */
 static double length_consistency(const trace_t *T, const node_t *nd, int l)
 {
     const orc_params *P = T->par;
     if (nd->hist_cnt < 2) { T->cnt->lc_cold++; return P->lc0; }
     T->cnt->lc_exp++;
-    double mu = (double)nd->hist_sum / (double)nd->hist_cnt;
+    double inv_c = 1.0 / (double)nd->hist_cnt;
+    double mu = (double)nd->hist_sum * inv_c;
     int64_t var_num = nd->hist_cnt * nd->hist_sumsq - nd->hist_sum * nd->hist_sum; /* cnt²·Var, exact */
-    double sigma = MAX(sqrt((double)var_num) / (double)nd->hist_cnt, P->sigma_floor);
-    double k = 0.5 / (sigma * sigma);                       /* 1/(2σ²) */
-    double c = 1.0 / (sigma * 0x1.40d931ff62705p+1);        /* 1/(σ√(2π)) */
+    double sigma = MAX(sqrt((double)var_num) * inv_c, P->sigma_floor);
+    double inv_s = 1.0 / sigma;
+    double k = (0.5 * inv_s) * inv_s;                       /* 1/(2σ²) */
+    double c = inv_s * 0x1.9884533d43651p-2;                /* 1/(σ√(2π)) */
     double d = (double)l - mu;
     return c * orc_exp_neg((d * d) * k);
 }

@@ -30,7 +30,6 @@ namespace {
 
 constexpr int kBlock = 128;                 // 4 warps per CTA
 using dev::kInf;
-using dev::kSqrt2Pi;
 using dev::task_batch;
 using dev::task_len;
 using dev::task_w;

@@ -42,7 +42,6 @@ constexpr int kLaneBlock = 128;
 using dev::dmax;
 using dev::dmin;
 using dev::kInf;
-using dev::kSqrt2Pi;
 using dev::task_batch;
 using dev::task_len;
 using dev::task_w;
@@ -377,12 +376,14 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                         SL_(best) = s1;
                         SL2_(best) = s2;
                         APREV_(best) = a;
-                        if (c >= 2) {
-                            MU_(best) = (double)s1 / (double)c;
+                        if (c >= 2) {   // cached Eq. 2 statistics (DESIGN.md R-stat)
+                            const double inv_c = 1.0 / (double)c;
+                            MU_(best) = (double)s1 * inv_c;
                             const long long var = (long long)c * s2 - s1 * s1;
-                            const double sigma = dmax(sqrt((double)var) / (double)c, p.sigma_floor);
-                            KK_(best) = 0.5 / (sigma * sigma);
-                            CC_(best) = 1.0 / (sigma * kSqrt2Pi);
+                            const double sigma = dmax(sqrt((double)var) * inv_c, p.sigma_floor);
+                            const double inv_s = 1.0 / sigma;
+                            KK_(best) = (0.5 * inv_s) * inv_s;
+                            CC_(best) = inv_s * dev::kInvSqrt2Pi;
                             warm |= 1u << best;
                         }
 #pragma unroll

@@ -39,7 +39,6 @@ namespace tile {
 
 constexpr int kBlock = 128;                 // 4 warps per CTA
 using dev::kInf;
-using dev::kSqrt2Pi;
 using dev::task_batch;
 using dev::task_len;
 using dev::task_w;
@@ -174,8 +173,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
         }
         if (!active) continue;   // (finished lanes only: back to the warp vote)
 
-        if (status == LMX_OK && (i < nI || j < nT) && ++iters > 2 * (nI + nT) + 2) status = LMX_EBUDGET;
-        const bool done_trace = (status != LMX_OK) || (i >= nI && j >= nT);
+        const bool more = (i < nI) | (j < nT);
+        iters += more;
+        if (more & (iters > 2 * (nI + nT) + 2)) status = LMX_EBUDGET;
+        const bool done_trace = (status != LMX_OK) | !more;
 
         if (done_trace) {
             // ---- per-trace metrics, node folds in node order ----
@@ -447,13 +448,15 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                                 cnt[jj]++;
                                 sl[jj] += l;
                                 sl2[jj] += (long long)l * l;
-                                if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (population mean / sigma)
+                                if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (DESIGN.md R-stat)
                                     const long long c = cnt[jj];
-                                    mu[jj] = (double)sl[jj] / (double)c;
+                                    const double inv_c = 1.0 / (double)c;
+                                    mu[jj] = (double)sl[jj] * inv_c;
                                     const long long var = c * sl2[jj] - sl[jj] * sl[jj];
-                                    const double sigma = dev::dmax(sqrt((double)var) / (double)c, p.sigma_floor);
-                                    kk[jj] = 0.5 / (sigma * sigma);
-                                    cc[jj] = 1.0 / (sigma * kSqrt2Pi);
+                                    const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
+                                    const double inv_s = 1.0 / sigma;
+                                    kk[jj] = (0.5 * inv_s) * inv_s;
+                                    cc[jj] = inv_s * dev::kInvSqrt2Pi;
                                 }
                             }
                         }
