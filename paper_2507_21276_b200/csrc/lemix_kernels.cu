@@ -102,7 +102,9 @@ int npl_bucket(int npl) { return tile::npl_bucket(npl); }
 int event_loop_smem_bytes(const KParams &p)
 {
     const int W = tile::window_entries(p.S);
-    return 16 * p.N * p.S + (W > 0 ? kBlock * npl_bucket(p.npl) * W * (p.S + 1) * 16 : 0);
+    const int npl = npl_bucket(p.npl);
+    return 16 * p.N * p.S + (W > 0 ? kBlock * npl * W * (p.S + 1) * 16 : 0) +
+           kBlock * npl * tile::cold_words(p.S) * 8;
 }
 
 int event_loop_block_threads() { return kBlock; }

@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
     const long long gthread = (long long)blockIdx.x * B + tid;
     const long long K = (long long)p.kmask + 1;
     const long long rb0 = gthread * NMAX * K;               // ring of node n: rb0 + n*K
-    const double2 *__restrict__ ring_be = p.ring_be;
+    double2 *ring_be = p.ring_be;   // written in this kernel: coherent loads only
 
     // ---- hot per-node state (registers) ----
     double P[NMAX][SMAX];
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             for (int s = 0; s < SMAX; ++s) sk[s] = SK_(n, s);
                             double II;
                             int gc;
-                            const dev::Ring q{ring_be + (rb0 + n * K) * (S + 1), p.kmask, S, nullptr, 0, 0};
+                            const dev::Ring q{ring_be + (rb0 + n * K) * (S + 1), p.kmask, S, 0u, 0u, 0};
                             dev::plan<SMAX, LMX_LANE_PF>(P[n], (hasp >> n) & 1u, S, s_ef + n * S, s_eb + n * S, q, qh[n], qn[n],
                                             sk, w, a, now, en[n], st0[n], II, gc);
 #pragma unroll
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     for (int s = 0; s < SMAX; ++s) sk[s] = SK_(best, s);
                     double II;
                     int gc;
-                    const dev::Ring q{ring_be + (rb0 + best * K) * (S + 1), p.kmask, S, nullptr, 0, 0};
+                    const dev::Ring q{ring_be + (rb0 + best * K) * (S + 1), p.kmask, S, 0u, 0u, 0};
                     dev::plan<SMAX, LMX_LANE_PF>(Pc, (hasp >> best) & 1u, S, s_ef + best * S, s_eb + best * S, q, qhc, qnc, sk,
                                     w, a, now, en_b, st0_b, II, gc);
 #pragma unroll
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                 for (int n = 1; n < NMAX; ++n)
                     if (n == best) { qhb = qh[n]; qnb = qn[n]; }
                 double2 *rbe = p.ring_be + (rb0 + best * K) * (S + 1);
-                const dev::Ring qb{rbe, p.kmask, S, nullptr, 0, 0};
+                const dev::Ring qb{rbe, p.kmask, S, 0u, 0u, 0};
 #pragma unroll
                 for (int s = 0; s < SMAX; ++s)
                     if (s < S) BUSY_(best, s) = BUSY_(best, s) + ef[s] * w;

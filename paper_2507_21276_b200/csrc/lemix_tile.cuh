@@ -28,10 +28,10 @@
 #define LMX_TILE_PF false                   // up-front ring loads in Alg. 1 (see dev::plan)
 #endif
 #ifndef LMX_TILE_WIN
-#define LMX_TILE_WIN 8                      // ring tail-window entries in shared memory (S <= 2)
+#define LMX_TILE_WIN 4                      // ring tail-window entries in shared memory (S <= 2)
 #endif
 #ifndef LMX_TILE_MINB
-#define LMX_TILE_MINB 3                     // resident CTAs/SM the register budget targets
+#define LMX_TILE_MINB 4                     // resident CTAs/SM the register budget targets
 #endif
 
 namespace lmx {
@@ -46,6 +46,8 @@ using dev::task_w;
 inline int stages_bucket(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16; }
 inline int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
 inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN : 0; }
+// 8-byte shared-memory words of commit-only state per node slot and thread
+inline int cold_words(int S) { return 2 * S + 3; }
 
 template <int SMAX, bool EXACT, int NPL, bool LEMIX>
 __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
@@ -82,20 +84,31 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     const long long gtile = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> log2T;
     const long long K = (long long)p.kmask + 1;
 
-    // the Q_train ring of each node this lane owns
-    // ring tail window (shared memory), [slot jj][W][S+1][thread]
+    // the Q_train ring of each node this lane owns: a shared-memory tail
+    // window, [slot jj][W][S+1][thread] (see dev::RingT), over a global ring
     constexpr int W = (SMAX <= 2) ? LMX_TILE_WIN : 0;   // see window_entries()
-    double2 *win[NPL];
-#pragma unroll
-    for (int jj = 0; jj < NPL; ++jj)
-        win[jj] = reinterpret_cast<double2 *>(smem_raw + 16 * NS) + (jj * (W > 0 ? W : 1) * (S + 1)) * blockDim.x +
-                  threadIdx.x;
+    const uint32_t wstride = 16u * blockDim.x;
+    uint32_t ws[NPL];
     double2 *rbe[NPL];
 #pragma unroll
     for (int jj = 0; jj < NPL; ++jj) {
+        ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * (S + 1)) * wstride +
+                 16u * threadIdx.x;
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
         rbe[jj] = p.ring_be + rbase * (S + 1);
     }
+    // commit-only per-node state in shared memory ("cold" words, 8 bytes each,
+    // [word][thread] so each thread owns a conflict-free column): per slot jj
+    // LB[s] (last planned backward end), busy[s], sum l, sum l^2, and
+    // (training count, version pointer) -- see cold_words()
+    const uint32_t cstride = 8u * blockDim.x;
+    const uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
+                           (uint32_t)(W > 0 ? NPL * W * (S + 1) : 0) * wstride + 8u * threadIdx.x;
+    auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + s) * cstride; };
+    auto c_busy = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + S + s) * cstride; };
+    auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S) * cstride; };
+    auto c_sl2 = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S + 1) * cstride; };
+    auto c_ntr = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S + 2) * cstride; };
 
     // ---- per-trace (tile-replicated) state ----
     bool active = false, finished = false;
@@ -110,11 +123,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     uint32_t v_inf = 0, v_inf2 = 0, v_tr = 0, v_tr2 = 0;
 
     // ---- per-node state of this lane's slots (registers) ----
-    double P[NPL][SMAX], LB[NPL][SMAX], busy[NPL][SMAX];
+    double P[NPL][SMAX];
     double aprev[NPL], mu[NPL], kk[NPL], cc[NPL];
-    int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL], ntr[NPL], vp[NPL];
+    int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL];
     int sk[NPL][SMAX];   // stale-prefix pointers (see dev::plan)
-    long long sl[NPL], sl2[NPL];
 
     // Control flow inside the loop is structured (no continue/break out of a
     // branch) so tiles that took different branches reconverge right after it.
@@ -153,15 +165,19 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 if (nT > 0) t_first = dev::dmin(t_first, a_tr);
 #pragma unroll
                 for (int jj = 0; jj < NPL; ++jj) {
-                    hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = ntr[jj] = vp[jj] = 0;
-                    sl[jj] = sl2[jj] = 0;
+                    hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = 0;
                     aprev[jj] = mu[jj] = kk[jj] = cc[jj] = 0.0;
+                    dev::sts_l(c_sl(jj), 0);
+                    dev::sts_l(c_sl2(jj), 0);
+                    dev::sts_l(c_ntr(jj), 0);      // training count | version pointer << 32
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s) {
                         P[jj][s] = 0.0;
-                        LB[jj][s] = -kInf;
-                        busy[jj][s] = 0.0;
                         sk[jj][s] = 0;
+                        if (s < S) {
+                            dev::sts_d(c_lb(jj, s), -kInf);
+                            dev::sts_d(c_busy(jj, s), 0.0);
+                        }
                     }
                 }
                 if (!LEMIX && p.policy == LMX_SEPARATE && N == 1 && nI > 0 && nT > 0) {
@@ -206,14 +222,18 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     long long c = 0, v2 = 0;
 #pragma unroll
                     for (int jj = 0; jj < NPL; ++jj)
-                        if (jj == jn) { c = cnt[jj]; v2 = (long long)cnt[jj] * sl2[jj] - sl[jj] * sl[jj]; }
+                        if (jj == jn) {
+                            const long long a1 = dev::lds_l(c_sl(jj)), a2 = dev::lds_l(c_sl2(jj));
+                            c = cnt[jj];
+                            v2 = (long long)cnt[jj] * a2 - a1 * a1;
+                        }
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s) {
                         if (s < S) {
                             double bv = 0.0;
 #pragma unroll
                             for (int jj = 0; jj < NPL; ++jj)
-                                if (jj == jn) bv = busy[jj][s];
+                                if (jj == jn) bv = dev::lds_d(c_busy(jj, s));
                             U = U + dev::shfl_d(tmask, bv, src);
                         }
                     }
@@ -340,7 +360,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         double II;
                         int gc;
                         const int qhead = qh[jj], qlen = qn[jj];
-                        const dev::RingT<W> q{rbe[jj], p.kmask, S, win[jj], (int)blockDim.x, qhead + qlen};
+                        const dev::RingT<W> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
                         dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
                                         a, now, en_s[jj], st0_s[jj], II, gc);
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
@@ -393,13 +413,16 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         if (jj == jb) {
                             const double *ef = s_ef + best * S;
                             const double *eb = s_eb + best * S;
-                            const dev::RingT<W> q{rbe[jj], p.kmask, S, win[jj], (int)blockDim.x, qh[jj] + qn[jj]};
+                            const dev::RingT<W> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
+                            double bz[SMAX];   // busy[s] (PAPER.md:787 utilisation), forward first
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
                                 if (s < S) {
                                     P[jj][s] = en_s[jj][s];
-                                    busy[jj][s] = busy[jj][s] + ef[s] * w;
+                                    bz[s] = dev::lds_d(c_busy(jj, s)) + ef[s] * w;
                                 }
+                            const long long trv = dev::lds_l(c_ntr(jj));
+                            int ntr = (int)(trv & 0xffffffffll), vp = (int)(trv >> 32);
                             hasp[jj] = 1;
                             aprev[jj] = a;
                             c_en0 = en_s[jj][0];
@@ -409,50 +432,51 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                                 c_status = LMX_EQCAP;
                             } else if (is_train) {
                                 // backward planning, stages S..1
-                                const int slot = (qh[jj] + qn[jj]) & p.kmask;
+                                double2 bw[SMAX];
                                 double x = c_done;
 #pragma unroll
                                 for (int s = SMAX - 1; s >= 0; --s) {
+                                    bw[s] = make_double2(0.0, 0.0);
                                     if (s < S) {
-                                        const double sb = dev::dmax(x, LB[jj][s]);
+                                        const double sb = dev::dmax(x, dev::lds_d(c_lb(jj, s)));
                                         const double ebv = sb + eb[s] * w;
-                                        LB[jj][s] = ebv;
-                                        rbe[jj][slot * (S + 1) + s] = make_double2(sb, ebv);
-                                        if (W > 0)
-                                            win[jj][(((qh[jj] + qn[jj]) & (W - 1)) * (S + 1) + s) * blockDim.x] =
-                                                make_double2(sb, ebv);
+                                        dev::sts_d(c_lb(jj, s), ebv);
+                                        bw[s] = make_double2(sb, ebv);
                                         x = ebv;
                                     }
                                 }
-                                rbe[jj][slot * (S + 1) + S] = make_double2(w, 0.0);
-                                if (W > 0)
-                                    win[jj][(((qh[jj] + qn[jj]) & (W - 1)) * (S + 1) + S) * blockDim.x] =
-                                        make_double2(w, 0.0);
+                                q.push<SMAX>(qh[jj], bw, w);
                                 qn[jj]++;
 #pragma unroll
                                 for (int s = 0; s < SMAX; ++s)
-                                    if (s < S) busy[jj][s] = busy[jj][s] + eb[s] * w;
-                                ntr[jj]++;
+                                    if (s < S) bz[s] = bz[s] + eb[s] * w;
+                                ntr++;
                                 c_done = x;
                             } else {
                                 // version-at-inference: completed backwards form a prefix of
                                 // Q_train; start_f^1 of successive commits on a node is
                                 // non-decreasing, so the boundary pointer only moves forward.
-                                int k = vp[jj] > qh[jj] ? vp[jj] : qh[jj];
+                                int k = vp > qh[jj] ? vp : qh[jj];
                                 const int tail = qh[jj] + qn[jj];
                                 while (k < tail && q.at(k, 0).y <= c_st0) k++;
-                                vp[jj] = k;
-                                c_ver = ntr[jj] - (tail - k);
+                                vp = k;
+                                c_ver = ntr - (tail - k);
                             }
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) dev::sts_d(c_busy(jj, s), bz[s]);
+                            dev::sts_l(c_ntr(jj), (long long)(unsigned)ntr | ((long long)vp << 32));
                             if (c_status == LMX_OK) {
                                 cnt[jj]++;
-                                sl[jj] += l;
-                                sl2[jj] += (long long)l * l;
+                                const long long sl = dev::lds_l(c_sl(jj)) + l;
+                                const long long sl2 = dev::lds_l(c_sl2(jj)) + (long long)l * l;
+                                dev::sts_l(c_sl(jj), sl);
+                                dev::sts_l(c_sl2(jj), sl2);
                                 if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (DESIGN.md R-stat)
                                     const long long c = cnt[jj];
                                     const double inv_c = 1.0 / (double)c;
-                                    mu[jj] = (double)sl[jj] * inv_c;
-                                    const long long var = c * sl2[jj] - sl[jj] * sl[jj];
+                                    mu[jj] = (double)sl * inv_c;
+                                    const long long var = c * sl2 - sl * sl;
                                     const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
                                     const double inv_s = 1.0 / sigma;
                                     kk[jj] = (0.5 * inv_s) * inv_s;
