@@ -49,7 +49,7 @@ inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN :
 // 8-byte shared-memory words of commit-only state per node slot and thread
 inline int cold_words(int S) { return 2 * S + 3; }
 
-template <int SMAX, bool EXACT, int NPL, bool LEMIX>
+template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT>
 __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
 {
     // LEMIX: the policy is LeMix (all candidates planned and scored); else one
@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
 
     // ---- tile geometry ----
     const int lane = threadIdx.x & 31;
-    const int T = p.T, log2T = p.log2T;
+    // TT > 0: the tile width is a compile-time constant (shuffle loops unroll)
+    const int T = TT > 0 ? TT : p.T, log2T = TT > 0 ? __builtin_ctz(TT > 0 ? TT : 1) : p.log2T;
     const int tl = lane & (T - 1);
     const int tbase = lane & ~(T - 1);
     const unsigned tmask = (T == 32) ? 0xffffffffu : (((1u << T) - 1u) << tbase);
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         m = dev::dmin(m, latest + s_ef[n * S + S - 1] * wn);
                     }
                 }
+                #pragma unroll
                 for (int off = T >> 1; off > 0; off >>= 1) m = dev::dmin(m, dev::shfl_xor_d(tmask, m, off));
                 double tauR;
                 if (p.slo_mode == 1) {
@@ -350,13 +352,30 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 double st0_s[NPL];
                 double f_best = 0.0;
                 int n_best = INT_MAX;
+                // Eq. 2 statistics of each owned node if this task is committed
+                // there (DESIGN.md R-stat), computed here by every lane -- where
+                // the work overlaps the other candidates' latency -- instead of
+                // serially by the winning lane in the commit
+                double mu_n[NPL], kk_n[NPL], cc_n[NPL];
+                long long sl_n[NPL], sl2_n[NPL];
 #pragma unroll
                 for (int jj = 0; jj < NPL; ++jj) {
                     const int n = tl + jj * T;
                     st0_s[jj] = 0.0;
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s) en_s[jj][s] = 0.0;
+                    mu_n[jj] = kk_n[jj] = cc_n[jj] = 0.0;
+                    sl_n[jj] = sl2_n[jj] = 0;
                     if (n < N && (LEMIX || n == chosen)) {
+                        // Eq. 2 of this candidate, ahead of (and
+                        // independent of) Algorithm 1; exp_neg is evaluated for cold
+                        // nodes too and discarded (its value is finite for t >= 0)
+                        double LC = p.lc0;
+                        if (LEMIX) {
+                            const double d = (double)l - mu[jj];
+                            const double lw = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
+                            LC = (cnt[jj] < 2) ? p.lc0 : lw;
+                        }
                         double II;
                         int gc;
                         const int qhead = qh[jj], qlen = qn[jj];
@@ -372,15 +391,22 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                             const double a_last = hasp[jj] ? aprev[jj] : a;               // R-9
                             const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
                             const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
-                            double LC;                                                    // Eq. 2
-                            if (cnt[jj] < 2) {
-                                LC = p.lc0;
-                            } else {
-                                const double d = (double)l - mu[jj];
-                                LC = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
-                            }
                             const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
                             if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
+                        }
+                        {   // speculative statistics: count cnt+1, sums + l, + l^2
+                            const long long c = cnt[jj] + 1;
+                            const long long a1 = dev::lds_l(c_sl(jj)) + l;
+                            const long long a2 = dev::lds_l(c_sl2(jj)) + (long long)l * l;
+                            sl_n[jj] = a1;
+                            sl2_n[jj] = a2;
+                            const double inv_c = 1.0 / (double)c;
+                            mu_n[jj] = (double)a1 * inv_c;
+                            const long long var = c * a2 - a1 * a1;
+                            const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
+                            const double inv_s = 1.0 / sigma;
+                            kk_n[jj] = (0.5 * inv_s) * inv_s;
+                            cc_n[jj] = inv_s * dev::kInvSqrt2Pi;
                         }
                     }
                 }
@@ -388,6 +414,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 // ---- a8: arg-best over the tile: highest f, then lowest node index ----
                 int best;
                 if (LEMIX) {
+#pragma unroll
                     for (int off = T >> 1; off > 0; off >>= 1) {
                         const double f2 = dev::shfl_xor_d(tmask, f_best, off);
                         const int n2 = __shfl_xor_sync(tmask, n_best, off);
@@ -467,32 +494,25 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                                 if (s < S) dev::sts_d(c_busy(jj, s), bz[s]);
                             dev::sts_l(c_ntr(jj), (long long)(unsigned)ntr | ((long long)vp << 32));
                             if (c_status == LMX_OK) {
+                                // cached Eq. 2 statistics (DESIGN.md R-stat), computed
+                                // speculatively above; unused while cnt < 2
                                 cnt[jj]++;
-                                const long long sl = dev::lds_l(c_sl(jj)) + l;
-                                const long long sl2 = dev::lds_l(c_sl2(jj)) + (long long)l * l;
-                                dev::sts_l(c_sl(jj), sl);
-                                dev::sts_l(c_sl2(jj), sl2);
-                                if (cnt[jj] >= 2) {   // cached Eq. 2 statistics (DESIGN.md R-stat)
-                                    const long long c = cnt[jj];
-                                    const double inv_c = 1.0 / (double)c;
-                                    mu[jj] = (double)sl * inv_c;
-                                    const long long var = c * sl2 - sl * sl;
-                                    const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
-                                    const double inv_s = 1.0 / sigma;
-                                    kk[jj] = (0.5 * inv_s) * inv_s;
-                                    cc[jj] = inv_s * dev::kInvSqrt2Pi;
-                                }
+                                dev::sts_l(c_sl(jj), sl_n[jj]);
+                                dev::sts_l(c_sl2(jj), sl2_n[jj]);
+                                mu[jj] = mu_n[jj];
+                                kk[jj] = kk_n[jj];
+                                cc[jj] = cc_n[jj];
                             }
                         }
                     }
                 }
+                if (c_status != LMX_OK) c_ver = INT_MIN;   // (a version count is never negative)
                 c_done = dev::shfl_d(tmask, c_done, owner);
                 c_en0 = dev::shfl_d(tmask, c_en0, owner);
-                c_st0 = dev::shfl_d(tmask, c_st0, owner);
+                if (p.node_defer) c_st0 = dev::shfl_d(tmask, c_st0, owner);
                 c_ver = __shfl_sync(tmask, c_ver, owner);
-                c_status = __shfl_sync(tmask, c_status, owner);
-                if (c_status != LMX_OK) {
-                    status = c_status;
+                if (c_ver == INT_MIN) {
+                    status = LMX_EQCAP;
                 } else {
                     // ---- a11: outputs + per-trace folds ----
                     if (tl == 0 && p.node_defer) {
@@ -554,9 +574,9 @@ template <int SMAX, bool EXACT, bool LEMIX>
 kernel_fn pick_npl(int npl)
 {
     switch (npl) {
-    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX>;
-    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX>;
-    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX>;
+    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX, 0>;
+    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX, 0>;
+    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX, 0>;
     }
 }
 
@@ -566,7 +586,10 @@ kernel_fn pick(const KParams &p)
     const int nb = npl_bucket(p.npl);
     switch (stages_bucket(p.S)) {
     case 1: return pick_npl<1, true, LEMIX>(nb);
-    case 2: return p.S == 2 ? pick_npl<2, true, LEMIX>(nb) : pick_npl<2, false, LEMIX>(nb);
+    case 2:
+        // the bench shape (4 nodes x 2 stages): tile width fixed at compile time
+        if (p.S == 2 && nb == 1 && p.T == 4) return event_loop_kernel<2, true, 1, LEMIX, 4>;
+        return p.S == 2 ? pick_npl<2, true, LEMIX>(nb) : pick_npl<2, false, LEMIX>(nb);
     case 4: return p.S == 4 ? pick_npl<4, true, LEMIX>(nb) : pick_npl<4, false, LEMIX>(nb);
     case 8: return p.S == 8 ? pick_npl<8, true, LEMIX>(nb) : pick_npl<8, false, LEMIX>(nb);
     default: return p.S == 16 ? pick_npl<16, true, LEMIX>(nb) : pick_npl<16, false, LEMIX>(nb);
