@@ -153,3 +153,43 @@ def test_rerun_reuses_streamed_inputs():
         assert a.tobytes() == b.tobytes()
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_sharded_runs_equal_single_run(world):
+    """SURVEY.md §8(e) / §4 "fake backend": the P strided shards bench.py's
+    ranks would own, run one after another on this GPU, reproduce the single
+    run's per-trace outputs bit for bit, and their host-side sum of the
+    per-cell blocks equals the single run's cells (integers exactly, fp64
+    within 1e-12 relative) -- the result the one NCCL all-reduce returns."""
+    from paper_2507_21276_b200 import dist as ldist
+    N, S = 4, 2
+    parts = [workload.generate(workload.sweep_spec(rate), 96, seed_base=500 + 96 * k)
+             for k, rate in enumerate(workload.SWEEP_RATES)]
+    tr = workload.concat(parts)
+    cells = np.repeat(np.arange(16, dtype=np.int32), 96)
+    lp = lemix.Params()
+    ef, eb = workload.profile(N, S)
+    whole = lemix.run(ef, eb, N, S, tr, lp, outputs=True, cells=cells, n_cells=16)
+    assert whole.status == 0
+    acc = None
+    for rank in range(world):
+        idx = ldist.strided_shard(tr.n_traces, rank, world)
+        sub = tr.subset(idx)
+        g = lemix.run(ef, eb, N, S, sub, lp, outputs=True, cells=cells[idx], n_cells=16)
+        assert g.status == 0
+        assert g.summaries.tobytes() == whole.summaries[idx].tobytes()
+        sel = np.concatenate([np.arange(tr.offsets[t], tr.offsets[t + 1]) for t in idx])
+        assert np.array_equal(g.node_defer, whole.node_defer[sel])
+        assert np.array_equal(g.decision_idx, whole.decision_idx[sel])
+        assert g.completion.tobytes() == whole.completion[sel].tobytes()
+        assert g.start_f1.tobytes() == whole.start_f1[sel].tobytes()
+        if acc is None:
+            acc = {k: g.cells[k].copy() for k in lemix.CELL_INT + lemix.CELL_F64}
+        else:
+            for k in lemix.CELL_INT + lemix.CELL_F64:
+                acc[k] = acc[k] + g.cells[k]
+    for k in lemix.CELL_INT:
+        assert np.array_equal(acc[k], whole.cells[k]), k
+    for k in lemix.CELL_F64:
+        np.testing.assert_allclose(acc[k], whole.cells[k], rtol=1e-12, err_msg=k)
