@@ -503,7 +503,7 @@ lmx_status lmx_run(lmx_ctx *c)
 
     // device buffers
     const size_t ring_entries = (size_t)tiles * k.npad * K;
-    if (c->ring_be.ensure(ring_entries * (c->S + 1) * sizeof(double2)) != cudaSuccess)
+    if (c->ring_be.ensure(ring_entries * lmx::ring_words(c->S) * sizeof(double2)) != cudaSuccess)
         return c->fail(LMX_ENOMEM, "queue ring allocation (" + std::to_string(ring_entries) + " entries; lower qcap)");
     if (c->summaries.ensure(std::max<int64_t>(T, 1) * sizeof(lmx_summary)) != cudaSuccess ||
         c->trace_err.ensure(std::max<int64_t>(T, 1) * 8) != cudaSuccess ||

@@ -7,6 +7,10 @@
 
 namespace lmx {
 
+// double2 words of one Q_train entry: (start_b, end_b) per stage, then the
+// backward durations in pairs (see dev::RingT)
+__host__ __device__ constexpr inline int ring_words(int S) { return S + (S + 1) / 2; }
+
 // Everything the persistent event-loop kernel needs, passed by value.
 struct KParams {
     // geometry of the candidate sweep: a "tile" of T lanes owns one trace,
@@ -42,7 +46,7 @@ struct KParams {
     unsigned long long *work;  // device [1]: next trace to claim
     unsigned long long *first_bad;  // device [1]: min failing trace index
 
-    double2 *ring_be;          // [tile_slots][Npad][K][S+1]: (start_b, end_b) per stage, (C*l^2, 0)
+    double2 *ring_be;          // [tile_slots][Npad][K][ring_words(S)]: (start_b, end_b) per stage, dB pairs
     int32_t npad;              // npl * T
 };
 

@@ -103,7 +103,7 @@ int event_loop_smem_bytes(const KParams &p)
 {
     const int W = tile::window_entries(p.S);
     const int npl = npl_bucket(p.npl);
-    return 16 * p.N * p.S + (W > 0 ? kBlock * npl * W * (p.S + 1) * 16 : 0) +
+    return 16 * p.N * p.S + (W > 0 ? kBlock * npl * W * ring_words(p.S) * 16 : 0) +
            kBlock * npl * tile::cold_words(p.S) * 8;
 }
 

@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             for (int s = 0; s < SMAX; ++s) sk[s] = SK_(n, s);
                             double II;
                             int gc;
-                            const dev::Ring q{ring_be + (rb0 + n * K) * (S + 1), p.kmask, S, 0u, 0u, 0};
+                            const dev::Ring q{ring_be + (rb0 + n * K) * ring_words(S), p.kmask, S, 0u, 0u, qh[n] + qn[n]};
                             dev::plan<SMAX, LMX_LANE_PF>(P[n], (hasp >> n) & 1u, S, s_ef + n * S, s_eb + n * S, q, qh[n], qn[n],
                                             sk, w, a, now, en[n], st0[n], II, gc);
 #pragma unroll
@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     for (int s = 0; s < SMAX; ++s) sk[s] = SK_(best, s);
                     double II;
                     int gc;
-                    const dev::Ring q{ring_be + (rb0 + best * K) * (S + 1), p.kmask, S, 0u, 0u, 0};
+                    const dev::Ring q{ring_be + (rb0 + best * K) * ring_words(S), p.kmask, S, 0u, 0u, qhc + qnc};
                     dev::plan<SMAX, LMX_LANE_PF>(Pc, (hasp >> best) & 1u, S, s_ef + best * S, s_eb + best * S, q, qhc, qnc, sk,
                                     w, a, now, en_b, st0_b, II, gc);
 #pragma unroll
@@ -324,8 +324,8 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
 #pragma unroll
                 for (int n = 1; n < NMAX; ++n)
                     if (n == best) { qhb = qh[n]; qnb = qn[n]; }
-                double2 *rbe = p.ring_be + (rb0 + best * K) * (S + 1);
-                const dev::Ring qb{rbe, p.kmask, S, 0u, 0u, 0};
+                double2 *rbe = p.ring_be + (rb0 + best * K) * ring_words(S);
+                const dev::Ring qb{rbe, p.kmask, S, 0u, 0u, qhb + qnb};
 #pragma unroll
                 for (int s = 0; s < SMAX; ++s)
                     if (s < S) BUSY_(best, s) = BUSY_(best, s) + ef[s] * w;
@@ -335,19 +335,23 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     status = LMX_EQCAP;
                 } else if (is_train) {
                     // backward planning, stages S..1
-                    const int slot = (qhb + qnb) & p.kmask;
+                    double2 bw[SMAX];
+                    double db[SMAX];
                     double x = done;
 #pragma unroll
                     for (int s = SMAX - 1; s >= 0; --s) {
+                        bw[s] = make_double2(0.0, 0.0);
+                        db[s] = 0.0;
                         if (s < S) {
                             const double sb = dmax(x, LB_(best, s));
-                            const double ebv = sb + eb[s] * w;
+                            db[s] = eb[s] * w;                 // dB_s (also line 16's offset)
+                            const double ebv = sb + db[s];
                             LB_(best, s) = ebv;
-                            rbe[slot * (S + 1) + s] = make_double2(sb, ebv);
+                            bw[s] = make_double2(sb, ebv);
                             x = ebv;
                         }
                     }
-                    rbe[slot * (S + 1) + S] = make_double2(w, 0.0);
+                    qb.push<SMAX>(qhb, bw, db);
                     qnb++;
 #pragma unroll
                     for (int n = 0; n < NMAX; ++n)

@@ -88,15 +88,15 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     // the Q_train ring of each node this lane owns: a shared-memory tail
     // window, [slot jj][W][S+1][thread] (see dev::RingT), over a global ring
     constexpr int W = (SMAX <= 2) ? LMX_TILE_WIN : 0;   // see window_entries()
-    const uint32_t wstride = 16u * blockDim.x;
+    constexpr uint32_t wstride = 16u * kBlock;            // (blockDim.x == kBlock)
     uint32_t ws[NPL];
     double2 *rbe[NPL];
 #pragma unroll
     for (int jj = 0; jj < NPL; ++jj) {
-        ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * (S + 1)) * wstride +
+        ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * ring_words(S)) * wstride +
                  16u * threadIdx.x;
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
-        rbe[jj] = p.ring_be + rbase * (S + 1);
+        rbe[jj] = p.ring_be + rbase * ring_words(S);
     }
     // commit-only per-node state in shared memory ("cold" words, 8 bytes each,
     // [word][thread] so each thread owns a conflict-free column): per slot jj
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     // (training count, version pointer) -- see cold_words()
     const uint32_t cstride = 8u * blockDim.x;
     const uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
-                           (uint32_t)(W > 0 ? NPL * W * (S + 1) : 0) * wstride + 8u * threadIdx.x;
+                           (uint32_t)(W > 0 ? NPL * W * ring_words(S) : 0) * wstride + 8u * threadIdx.x;
     auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + s) * cstride; };
     auto c_busy = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + S + s) * cstride; };
     auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S) * cstride; };
@@ -379,7 +379,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         double II;
                         int gc;
                         const int qhead = qh[jj], qlen = qn[jj];
-                        const dev::RingT<W> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
+                        const dev::RingT<W, wstride> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
                         dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
                                         a, now, en_s[jj], st0_s[jj], II, gc);
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         if (jj == jb) {
                             const double *ef = s_ef + best * S;
                             const double *eb = s_eb + best * S;
-                            const dev::RingT<W> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
+                            const dev::RingT<W, wstride> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
                             double bz[SMAX];   // busy[s] (PAPER.md:787 utilisation), forward first
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
@@ -460,19 +460,22 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                             } else if (is_train) {
                                 // backward planning, stages S..1
                                 double2 bw[SMAX];
+                                double db[SMAX];
                                 double x = c_done;
 #pragma unroll
                                 for (int s = SMAX - 1; s >= 0; --s) {
                                     bw[s] = make_double2(0.0, 0.0);
+                                    db[s] = 0.0;
                                     if (s < S) {
                                         const double sb = dev::dmax(x, dev::lds_d(c_lb(jj, s)));
-                                        const double ebv = sb + eb[s] * w;
+                                        db[s] = eb[s] * w;                 // dB_s (also line 16's offset)
+                                        const double ebv = sb + db[s];
                                         dev::sts_d(c_lb(jj, s), ebv);
                                         bw[s] = make_double2(sb, ebv);
                                         x = ebv;
                                     }
                                 }
-                                q.push<SMAX>(qh[jj], bw, w);
+                                q.push<SMAX>(qh[jj], bw, db);
                                 qn[jj]++;
 #pragma unroll
                                 for (int s = 0; s < SMAX; ++s)
