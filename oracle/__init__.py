@@ -33,11 +33,13 @@ class Params(ctypes.Structure):
                 ("slo_mode", ctypes.c_int32), ("qcap", ctypes.c_int32),
                 ("lambda1", ctypes.c_double), ("lambda2", ctypes.c_double), ("tau", ctypes.c_double),
                 ("slo_mult", ctypes.c_double), ("slo_const", ctypes.c_double),
-                ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double)]
+                ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("mem_enable", ctypes.c_int32), ("mem_pad", ctypes.c_int32), ("mem_cap", ctypes.c_int64),
+                ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes",
-               "sum_version", "status")
+               "sum_version", "status", "n_mem_wait", "n_offload")
 SUMMARY_F64 = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util",
                "mean_len_std")
 
@@ -91,11 +93,18 @@ class OracleParams:
     slo_mode: int = 0
     qcap: int = 512
     slo_const: float = 0.0
+    # Algorithm 2 (NEXT-1, DESIGN.md R-mem); mem_enable = 0: unlimited memory
+    mem_enable: int = 0
+    mem_cap: int = 0
+    mem_dt: float = 0.0
+    mem_tmax: float = 0.0
+    mem_pen: float = 0.0
 
     def _c(self) -> Params:
         return Params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1,
                       self.lambda2, self.tau, self.slo_mult, self.slo_const, self.sigma_floor,
-                      self.lc0, self.alpha)
+                      self.lc0, self.alpha, self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax,
+                      self.mem_pen)
 
 
 def _ptr(a):

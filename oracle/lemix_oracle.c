@@ -16,6 +16,7 @@
  *                              previous training task's S1 forward end PAPER.md:224 (§3)
  *   - baselines Separate / NaiveMix(RR)                                PAPER.md:795-796 (§6.1)
  *   - metrics (throughput, SLO = TTFT <= 5x forward latency)          PAPER.md:786-790 (§6.1)
+ *   - ExecuteTaskMemoryAware   Algorithm 2, lines 1-20 (optional)      PAPER.md:608-641 (§4.4)
  *
  * Where the paper is silent or garbled the DESIGN.md reading is cited as
  * [R-n] (DESIGN.md §"Readings").  Floating point: IEEE binary64, built with
@@ -77,6 +78,7 @@ double orc_exp_neg(double t)
 typedef struct {
     double sf[MAXS], ef[MAXS];   /* forward path  start_f^s, end_f^s */
     double sb[MAXS], eb[MAXS];   /* backward path start_b^s, end_b^s (training only) */
+    int off[MAXS];               /* Algorithm 2: activations offloaded from GPU s (line 10) */
 } path_t;
 
 typedef struct {
@@ -281,6 +283,104 @@ static void plan_backward(trace_t *T, int n, uint32_t v, path_t *p)
     }
 }
 
+/* ---------------------------------------------------------------------------
+ * Algorithm 2  ExecuteTaskMemoryAware, for the task just
+ * placed on node n, under the memory model of DESIGN.md [R-mem]:
+ *   - a forward of a task on stage s needs C*l tokens of activation memory
+ *     on GPU (n, s); a training task holds them until its stage-s backward
+ *     ends, an inference task releases them when its forward ends;
+ *   - MemoryAvailable(n, s) at time t (line 7): the tokens held at t by the
+ *     training tasks in Q_train^n (end_b^s > t, not offloaded from s) plus
+ *     the task's own need fit in mem_cap (= M_threshold, in tokens);
+ *   - lines 6-11: wait in steps of Delta_t; once the wait reaches T_max the
+ *     task's activations on s are offloaded (it then needs 0 tokens there)
+ *     and its forward on s takes mem_pen seconds per offloaded token longer;
+ *   - lines 12-14: Forward at the planned start plus the wait; calibration:
+ *     the executed interval replaces the planned one -- a forward that was
+ *     planned into the gap before a pending backward and no longer fits is
+ *     postponed past it exactly as Algorithm 1 lines 10-14 do;
+ *   - lines 15-17: the backward is planned after the executed forward path
+ *     (plan_backward), so the queues hold executed times.
+ * Only forwards are gated (Algorithm 2 checks memory before Forward only).
+ * With no waits the executed path equals Algorithm 1's plan.
+ * Writes the executed forward path to sf/ef and the offload flags to off;
+ * returns the number of stages that waited (the offloads are in off).
+ * ------------------------------------------------------------------------- */
+static int memory_available(const trace_t *T, int n, int s, double t, int64_t need)
+{
+    const node_t *nd = &T->node[n];
+    int64_t held = 0;
+    for (int64_t k = 0; k < nd->q_len; ++k) {
+        const path_t *q = &T->path[nd->q_train[k]];
+        if (q->eb[s] > t && !q->off[s]) {
+            uint32_t v = T->lbk[nd->q_train[k]];
+            held += (int64_t)task_batch(v) * task_len(v);
+        }
+    }
+    return held + need <= T->par->mem_cap;
+}
+
+static int execute_memory_aware(trace_t *T, int n, uint32_t v, double a, double *sf, double *ef, int *off)
+{
+    const int S = T->S;
+    const orc_params *P = T->par;
+    node_t *nd = &T->node[n];
+    const double w = task_w(v);
+    const int64_t tok = (int64_t)task_batch(v) * task_len(v);
+    double prev_ef[MAXS];
+    if (nd->last_task >= 0) {
+        for (int s = 0; s < S; ++s) prev_ef[s] = T->path[nd->last_task].ef[s];
+    } else {
+        double x = a;
+        for (int s = 0; s < S; ++s) { prev_ef[s] = x; x = x + eta_f(T, n, s) * w; }
+    }
+    int64_t front = 0;                                   /* Q_temp cursor over Q_train^n */
+    int waited = 0;
+    double e = a;
+    for (int s = 0; s < S; ++s) {
+        const double dF = eta_f(T, n, s) * w;
+        double start = MAX(e, prev_ef[s]);               /* Alg. 1 lines 5-6: planned start */
+        double end = start + dF;
+        while (front < nd->q_len) {                      /* Alg. 1 lines 8-14 */
+            const path_t *q = &T->path[nd->q_train[front]];
+            if (end <= q->sb[s]) break;
+            start = MAX(start, q->eb[s]);
+            end = start + dF;
+            front++;
+        }
+        /* Alg. 2 lines 6-11: wait-or-drop before Forward(task, s) */
+        double wait = 0.0;
+        off[s] = 0;
+        while (!memory_available(T, n, s, start + wait, tok)) {   /* line 7 */
+            wait = wait + P->mem_dt;                               /* line 8 */
+            if (wait >= P->mem_tmax) {                             /* line 9 */
+                off[s] = 1;                                        /* line 10: offload */
+                break;                                             /* line 11 */
+            }
+        }
+        /* line 12: after an offload the task needs no memory on GPU s, and the
+         * tokens held never exceed mem_cap (every admission was checked), so
+         * the check holds and the forward runs (see DESIGN.md [R-mem]). */
+        if (wait > 0.0) {
+            waited++;
+            const double dur = off[s] ? dF + P->mem_pen * (double)tok : dF;
+            start = start + wait;                        /* lines 13-14: calibrate */
+            end = start + dur;
+            while (front < nd->q_len) {                  /* no overlap with pending backwards */
+                const path_t *q = &T->path[nd->q_train[front]];
+                if (end <= q->sb[s]) break;
+                start = MAX(start, q->eb[s]);
+                end = start + dur;
+                front++;
+            }
+        }
+        sf[s] = start;
+        ef[s] = end;
+        e = end;
+    }
+    return waited;
+}
+
 int orc_run_trace(const orc_profile *prof, const orc_params *par,
                   int64_t n_tasks, int64_t n_inf,
                   const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
@@ -300,6 +400,9 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 
     /* ---- input validation (inputs must be finite, ordered and in range) ---- */
     int bad = (N < 1 || S < 1 || S > MAXS || nI < 0 || nT < 0 || par->qcap < 1 || !(par->lambda1 > 0.0));
+    if (par->mem_enable)   /* Delta_t > 0 and T_max finite bound the wait loop */
+        bad = bad || par->mem_cap < 0 || !(par->mem_dt > 0.0) || !(par->mem_tmax > 0.0 && par->mem_tmax < INFINITY) ||
+              !(par->mem_pen >= 0.0 && par->mem_pen < INFINITY) || par->mem_tmax / par->mem_dt > 1048576.0;
     for (int k = 0; k < N * S && !bad; ++k)
         bad = !(prof->eta_f[k] > 0.0 && prof->eta_f[k] < INFINITY && prof->eta_b[k] > 0.0 && prof->eta_b[k] < INFINITY);
     for (int64_t t = 0; t < n_tasks && !bad; ++t) {
@@ -423,9 +526,20 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 
         /* ---- commit: the task joins Q^best ---- */
         node_t *nd = &T.node[best];
-        for (int s = 0; s < S; ++s) { p->sf[s] = sfv[best][s]; p->ef[s] = efv[best][s]; }
         const double w = task_w(v);
-        for (int s = 0; s < S; ++s) nd->busy[s] = nd->busy[s] + eta_f(&T, best, s) * w;
+        if (par->mem_enable) {
+            /* Algorithm 2: execute (wait-or-drop) and calibrate */
+            sm.n_mem_wait += execute_memory_aware(&T, best, v, a, p->sf, p->ef, p->off);
+            for (int s = 0; s < S; ++s) {
+                sm.n_offload += p->off[s];
+                const double dF = eta_f(&T, best, s) * w;
+                const double dur = p->off[s] ? dF + par->mem_pen * (double)((int64_t)task_batch(v) * task_len(v)) : dF;
+                nd->busy[s] = nd->busy[s] + dur;
+            }
+        } else {
+            for (int s = 0; s < S; ++s) { p->sf[s] = sfv[best][s]; p->ef[s] = efv[best][s]; p->off[s] = 0; }
+            for (int s = 0; s < S; ++s) nd->busy[s] = nd->busy[s] + eta_f(&T, best, s) * w;
+        }
         double done;
         if (is_train) {
             if (nd->q_len >= par->qcap) { status = ORC_EQCAP; break; }

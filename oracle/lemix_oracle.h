@@ -37,11 +37,21 @@ typedef struct {
     double slo_mult, slo_const;     /* tau_R */
     double sigma_floor, lc0;        /* Eq. 2 singular cases */
     double alpha;                   /* Separate's training fraction */
+    /* Algorithm 2 ExecuteTaskMemoryAware (
+     * DESIGN.md reading R-mem).  mem_enable = 0: unlimited memory, the
+     * executed path is the planned one. */
+    int32_t mem_enable;
+    int32_t mem_pad;
+    int64_t mem_cap;                /* activation memory per stage GPU, in tokens (C*l units) */
+    double mem_dt;                  /* check interval Delta_t */
+    double mem_tmax;                /* maximum wait T_max */
+    double mem_pen;                 /* offload penalty, seconds per offloaded token */
 } orc_params;
 
 /* Per-trace summary.  Integer block then fp64 block. */
 typedef struct {
     int64_t n_tasks, n_inf, n_train, n_slo_met, n_deferrals, active_nodes, sum_version, status;
+    int64_t n_mem_wait, n_offload;  /* stage forwards that waited for memory / were offloaded (Alg. 2) */
     double makespan, throughput, sum_ttft, mean_ttft, slo_attainment, mean_util, mean_len_std;
 } orc_summary;
 
