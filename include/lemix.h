@@ -112,6 +112,21 @@ typedef struct {
     double sigma_floor;    /* Eq. 2 σ floor, > 0 */
     double lc0;            /* Eq. 2 value for nodes with < 2 tasks of history */
     double alpha;          /* Separate: N_train = clamp(floor(N·α + 0.5), 1, N-1), α in [0, 1] */
+    /* Algorithm 2 ExecuteTaskMemoryAware (DESIGN.md R-mem;
+     * SURVEY.md §8f NEXT-1).  0 (default): unlimited memory -- the executed
+     * path is Algorithm 1's plan.  1: before each stage forward the committed
+     * task waits in mem_dt steps until the activation tokens (C·ℓ) held on
+     * that GPU by queued training tasks plus its own fit in mem_cap; once the
+     * wait reaches mem_tmax its activations are offloaded (forward longer by
+     * mem_pen s per token) and it runs; the executed path replaces the plan
+     * (calibration).  Invalid values (mem_cap < 0, mem_dt <= 0, mem_tmax not
+     * finite and > 0, mem_tmax / mem_dt > 2^20, mem_pen < 0) -> LMX_EINVAL. */
+    int32_t mem_enable;
+    int32_t mem_pad;       /* zero */
+    int64_t mem_cap;       /* M_threshold per stage GPU, in activation tokens (C·ℓ units) */
+    double mem_dt;         /* check interval Δ_t, seconds */
+    double mem_tmax;       /* maximum wait T_max, seconds */
+    double mem_pen;        /* offload penalty, seconds per offloaded token */
 } lmx_params;
 
 /* Per-trace summary (metrics of PAPER.md:786-790).  For a trace whose status
@@ -123,6 +138,8 @@ typedef struct {
     int64_t active_nodes;   /* nodes that ran >= 1 task (consolidation) */
     int64_t sum_version;    /* Σ over inference tasks of the node's completed-training count */
     int64_t status;         /* lmx_status of this trace */
+    int64_t n_mem_wait;     /* Algorithm 2: stage forwards that waited for memory */
+    int64_t n_offload;      /* Algorithm 2: stage forwards whose activations were offloaded */
     double makespan;        /* last completion - first arrival */
     double throughput;      /* tasks / makespan */
     double sum_ttft, mean_ttft;

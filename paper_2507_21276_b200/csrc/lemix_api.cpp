@@ -191,6 +191,12 @@ void lmx_params_default(lmx_params *p)
     p->sigma_floor = 1.0;
     p->lc0 = 0.0;
     p->alpha = 0.5;
+    p->mem_enable = 0;     // unlimited memory: the executed path is the plan
+    p->mem_pad = 0;
+    p->mem_cap = 0;
+    p->mem_dt = 0.0;
+    p->mem_tmax = 0.0;
+    p->mem_pen = 0.0;
 }
 
 lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
@@ -373,6 +379,14 @@ lmx_status lmx_set_params(lmx_ctx *c, const lmx_params *p)
     if (!(p->sigma_floor > 0.0 && std::isfinite(p->sigma_floor))) return c->fail(LMX_EINVAL, "params.sigma_floor must be finite and > 0");
     if (!std::isfinite(p->lc0)) return c->fail(LMX_EINVAL, "params.lc0 must be finite");
     if (!(p->alpha >= 0.0 && p->alpha <= 1.0)) return c->fail(LMX_EINVAL, "params.alpha must be in [0, 1]");
+    if (p->mem_enable != 0 && p->mem_enable != 1) return c->fail(LMX_EINVAL, "params.mem_enable must be 0 or 1");
+    if (p->mem_enable) {   // Algorithm 2: Delta_t > 0 and a finite T_max bound the wait loop
+        if (p->mem_cap < 0) return c->fail(LMX_EINVAL, "params.mem_cap must be >= 0");
+        if (!(p->mem_dt > 0.0 && std::isfinite(p->mem_dt))) return c->fail(LMX_EINVAL, "params.mem_dt must be finite and > 0");
+        if (!(p->mem_tmax > 0.0 && std::isfinite(p->mem_tmax))) return c->fail(LMX_EINVAL, "params.mem_tmax must be finite and > 0");
+        if (!(p->mem_pen >= 0.0 && std::isfinite(p->mem_pen))) return c->fail(LMX_EINVAL, "params.mem_pen must be finite and >= 0");
+        if (p->mem_tmax / p->mem_dt > 1048576.0) return c->fail(LMX_EINVAL, "params.mem_tmax / mem_dt must be <= 2^20");
+    }
     c->par = *p;
     c->have_params = true;
     c->ran = false;
@@ -461,6 +475,11 @@ lmx_status lmx_run(lmx_ctx *c)
     k.slo_const = P.slo_const;
     k.sigma_floor = P.sigma_floor;
     k.lc0 = P.lc0;
+    k.mem_enable = P.mem_enable;
+    k.mem_cap = P.mem_cap;
+    k.mem_dt = P.mem_dt;
+    k.mem_tmax = P.mem_tmax;
+    k.mem_pen = P.mem_pen;
     k.n_traces = T;
     k.offsets = (const int64_t *)c->offsets.p;
     k.n_inf = (const int32_t *)c->n_inf.p;
@@ -476,6 +495,8 @@ lmx_status lmx_run(lmx_ctx *c)
         if (!strcmp(force, "lane")) {
             if (!lmx::lane_supported(c->N, c->S))
                 return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: not supported for this N x S");
+            if (P.mem_enable)
+                return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: the memory model (Algorithm 2) runs on the tile kernel only");
             lane = true;
         }
     }
@@ -503,7 +524,7 @@ lmx_status lmx_run(lmx_ctx *c)
 
     // device buffers
     const size_t ring_entries = (size_t)tiles * k.npad * K;
-    if (c->ring_be.ensure(ring_entries * lmx::ring_words(c->S) * sizeof(double2)) != cudaSuccess)
+    if (c->ring_be.ensure(ring_entries * lmx::ring_words(c->S, P.mem_enable != 0) * sizeof(double2)) != cudaSuccess)
         return c->fail(LMX_ENOMEM, "queue ring allocation (" + std::to_string(ring_entries) + " entries; lower qcap)");
     if (c->summaries.ensure(std::max<int64_t>(T, 1) * sizeof(lmx_summary)) != cudaSuccess ||
         c->trace_err.ensure(std::max<int64_t>(T, 1) * 8) != cudaSuccess ||

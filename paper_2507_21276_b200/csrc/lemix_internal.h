@@ -9,7 +9,8 @@ namespace lmx {
 
 // double2 words of one Q_train entry: (start_b, end_b) per stage, then the
 // backward durations in pairs (see dev::RingT)
-__host__ __device__ constexpr inline int ring_words(int S) { return S + (S + 1) / 2; }
+// (+ one word (C*l tokens, offload mask) with the memory model of Algorithm 2)
+__host__ __device__ constexpr inline int ring_words(int S, bool mem = false) { return S + (S + 1) / 2 + (mem ? 1 : 0); }
 
 // Everything the persistent event-loop kernel needs, passed by value.
 struct KParams {
@@ -23,6 +24,10 @@ struct KParams {
     int32_t s_pow2;      // S is a power of two -> II/S == II * (1/S) exactly
     double inv_S;
     double lambda1, lambda2, tau, slo_mult, slo_const, sigma_floor, lc0;
+    // Algorithm 2 (lmx_params.mem_*): the MEM kernel instantiations read these
+    int32_t mem_enable;
+    long long mem_cap;
+    double mem_dt, mem_tmax, mem_pen;
 
     int64_t n_traces;
     const int64_t *offsets;    // device [n_traces+1]

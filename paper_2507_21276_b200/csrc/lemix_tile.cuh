@@ -49,11 +49,13 @@ inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN :
 // 8-byte shared-memory words of commit-only state per node slot and thread
 inline int cold_words(int S) { return 2 * S + 3; }
 
-template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT>
+template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, bool MEM>
 __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
 {
     // LEMIX: the policy is LeMix (all candidates planned and scored); else one
     // of the baselines (RR / Separate / Fixed) picks the node first.
+    // MEM: the committed task is executed under Algorithm 2's memory model
+    // (dev::execute_mem) and the executed path replaces the plan.
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t s_bar;
 
@@ -93,10 +95,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     double2 *rbe[NPL];
 #pragma unroll
     for (int jj = 0; jj < NPL; ++jj) {
-        ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * ring_words(S)) * wstride +
+        ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * ring_words(S, MEM)) * wstride +
                  16u * threadIdx.x;
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
-        rbe[jj] = p.ring_be + rbase * ring_words(S);
+        rbe[jj] = p.ring_be + rbase * ring_words(S, MEM);
     }
     // commit-only per-node state in shared memory ("cold" words, 8 bytes each,
     // [word][thread] so each thread owns a conflict-free column): per slot jj
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     // (training count, version pointer) -- see cold_words()
     const uint32_t cstride = 8u * blockDim.x;
     const uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
-                           (uint32_t)(W > 0 ? NPL * W * ring_words(S) : 0) * wstride + 8u * threadIdx.x;
+                           (uint32_t)(W > 0 ? NPL * W * ring_words(S, MEM) : 0) * wstride + 8u * threadIdx.x;
     auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + s) * cstride; };
     auto c_busy = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + S + s) * cstride; };
     auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S) * cstride; };
@@ -120,6 +122,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     int cur_defer = 0, status = LMX_OK, err_task = 0, err_code = kErrNone;
     double r = kInf, t_first = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
     long long n_slo = 0, sum_ver = 0, n_def = 0;
+    int n_mwait = 0, n_moff = 0;          // Algorithm 2 counters (MEM)
     double a_inf = 0.0, a_inf2 = 0.0, a_tr = 0.0, a_tr2 = 0.0;   // 2-deep input prefetch
     uint32_t v_inf = 0, v_inf2 = 0, v_tr = 0, v_tr2 = 0;
 
@@ -153,6 +156,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 err_task = 0;
                 err_code = kErrNone;
                 n_slo = sum_ver = n_def = 0;
+                n_mwait = n_moff = 0;
                 sum_ttft = 0.0;
                 t_last = -kInf;
                 a_last_inf = -kInf;
@@ -203,6 +207,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
             sm.n_train = nT;
             sm.status = status;
             sm.n_slo_met = sm.n_deferrals = sm.active_nodes = sm.sum_version = 0;
+            sm.n_mem_wait = sm.n_offload = 0;
             sm.makespan = sm.throughput = sm.sum_ttft = sm.mean_ttft = sm.slo_attainment = 0.0;
             sm.mean_util = sm.mean_len_std = 0.0;
             if (status == LMX_OK) {
@@ -210,6 +215,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 sm.n_slo_met = n_slo;
                 sm.n_deferrals = n_def;
                 sm.sum_version = sum_ver;
+                sm.n_mem_wait = n_mwait;
+                sm.n_offload = n_moff;
                 sm.sum_ttft = sum_ttft;
                 sm.makespan = (ntask > 0) ? t_last - t_first : 0.0;
                 sm.throughput = (sm.makespan > 0.0) ? (double)ntask / sm.makespan : 0.0;
@@ -379,7 +386,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         double II;
                         int gc;
                         const int qhead = qh[jj], qlen = qn[jj];
-                        const dev::RingT<W, wstride> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
+                        const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
                         dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
                                         a, now, en_s[jj], st0_s[jj], II, gc);
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
@@ -433,20 +440,34 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 const int owner = tbase + (best & (T - 1));
                 const int jb = best >> log2T;
                 double c_done = 0.0, c_en0 = 0.0, c_st0 = 0.0;
-                int c_ver = 0, c_status = LMX_OK;
+                int c_ver = 0, c_status = LMX_OK, c_mem = 0;
                 if (lane == owner) {
 #pragma unroll
                     for (int jj = 0; jj < NPL; ++jj) {
                         if (jj == jb) {
                             const double *ef = s_ef + best * S;
                             const double *eb = s_eb + best * S;
-                            const dev::RingT<W, wstride> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
+                            const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
+                            const long long tok = (long long)task_batch(v) * l;   // activation tokens C*l
+                            int offm = 0;
+                            if (MEM) {
+                                // Algorithm 2: the executed path replaces the plan (calibration)
+                                double ex_st[SMAX];
+                                int nw = 0;
+                                dev::execute_mem<SMAX>(P[jj], hasp[jj] != 0, S, ef, q, qh[jj], qn[jj], w, tok, a,
+                                                       p.mem_cap, p.mem_dt, p.mem_tmax, p.mem_pen, ex_st, en_s[jj],
+                                                       offm, nw);
+                                st0_s[jj] = ex_st[0];
+                                c_mem = nw | (__popc(offm) << 8);
+                            }
                             double bz[SMAX];   // busy[s] (PAPER.md:787 utilisation), forward first
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
                                 if (s < S) {
                                     P[jj][s] = en_s[jj][s];
-                                    bz[s] = dev::lds_d(c_busy(jj, s)) + ef[s] * w;
+                                    const double dFs = ef[s] * w;
+                                    const double dur = (MEM && ((offm >> s) & 1)) ? dFs + p.mem_pen * (double)tok : dFs;
+                                    bz[s] = dev::lds_d(c_busy(jj, s)) + dur;
                                 }
                             const long long trv = dev::lds_l(c_ntr(jj));
                             int ntr = (int)(trv & 0xffffffffll), vp = (int)(trv >> 32);
@@ -475,7 +496,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                                         x = ebv;
                                     }
                                 }
-                                q.push<SMAX>(qh[jj], bw, db);
+                                q.push<SMAX>(qh[jj], bw, db, make_double2((double)tok, (double)offm));
                                 qn[jj]++;
 #pragma unroll
                                 for (int s = 0; s < SMAX; ++s)
@@ -514,6 +535,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 c_en0 = dev::shfl_d(tmask, c_en0, owner);
                 if (p.node_defer) c_st0 = dev::shfl_d(tmask, c_st0, owner);
                 c_ver = __shfl_sync(tmask, c_ver, owner);
+                if (MEM) {
+                    c_mem = __shfl_sync(tmask, c_mem, owner);
+                    if (c_ver != INT_MIN) { n_mwait += c_mem & 0xff; n_moff += c_mem >> 8; }
+                }
                 if (c_ver == INT_MIN) {
                     status = LMX_EQCAP;
                 } else {
@@ -573,29 +598,29 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
 
 typedef void (*kernel_fn)(const KParams);
 
-template <int SMAX, bool EXACT, bool LEMIX>
+template <int SMAX, bool EXACT, bool LEMIX, bool MEM>
 kernel_fn pick_npl(int npl)
 {
     switch (npl) {
-    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX, 0>;
-    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX, 0>;
-    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX, 0>;
+    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX, 0, MEM>;
+    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX, 0, MEM>;
+    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX, 0, MEM>;
     }
 }
 
-template <bool LEMIX>
+template <bool LEMIX, bool MEM>
 kernel_fn pick(const KParams &p)
 {
     const int nb = npl_bucket(p.npl);
     switch (stages_bucket(p.S)) {
-    case 1: return pick_npl<1, true, LEMIX>(nb);
+    case 1: return pick_npl<1, true, LEMIX, MEM>(nb);
     case 2:
         // the bench shape (4 nodes x 2 stages): tile width fixed at compile time
-        if (p.S == 2 && nb == 1 && p.T == 4) return event_loop_kernel<2, true, 1, LEMIX, 4>;
-        return p.S == 2 ? pick_npl<2, true, LEMIX>(nb) : pick_npl<2, false, LEMIX>(nb);
-    case 4: return p.S == 4 ? pick_npl<4, true, LEMIX>(nb) : pick_npl<4, false, LEMIX>(nb);
-    case 8: return p.S == 8 ? pick_npl<8, true, LEMIX>(nb) : pick_npl<8, false, LEMIX>(nb);
-    default: return p.S == 16 ? pick_npl<16, true, LEMIX>(nb) : pick_npl<16, false, LEMIX>(nb);
+        if (p.S == 2 && nb == 1 && p.T == 4) return event_loop_kernel<2, true, 1, LEMIX, 4, MEM>;
+        return p.S == 2 ? pick_npl<2, true, LEMIX, MEM>(nb) : pick_npl<2, false, LEMIX, MEM>(nb);
+    case 4: return p.S == 4 ? pick_npl<4, true, LEMIX, MEM>(nb) : pick_npl<4, false, LEMIX, MEM>(nb);
+    case 8: return p.S == 8 ? pick_npl<8, true, LEMIX, MEM>(nb) : pick_npl<8, false, LEMIX, MEM>(nb);
+    default: return p.S == 16 ? pick_npl<16, true, LEMIX, MEM>(nb) : pick_npl<16, false, LEMIX, MEM>(nb);
     }
 }
 

@@ -45,11 +45,13 @@ class lmx_params(ctypes.Structure):
     _fields_ = [("policy", ctypes.c_int32), ("deprioritize", ctypes.c_int32), ("slo_mode", ctypes.c_int32),
                 ("qcap", ctypes.c_int32), ("lambda1", ctypes.c_double), ("lambda2", ctypes.c_double),
                 ("tau", ctypes.c_double), ("slo_mult", ctypes.c_double), ("slo_const", ctypes.c_double),
-                ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double)]
+                ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double),
+                ("mem_enable", ctypes.c_int32), ("mem_pad", ctypes.c_int32), ("mem_cap", ctypes.c_int64),
+                ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version",
-               "status")
+               "status", "n_mem_wait", "n_offload")
 SUMMARY_F64 = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util",
                "mean_len_std")
 SUMMARY_DTYPE = np.dtype([(k, np.int64) for k in SUMMARY_INT] + [(k, np.float64) for k in SUMMARY_F64])
@@ -133,10 +135,17 @@ class Params:
     sigma_floor: float = 1.0
     lc0: float = 0.0
     alpha: float = 0.5
+    # Algorithm 2 memory model (include/lemix.h lmx_params.mem_*); 0 = unlimited memory
+    mem_enable: int = 0
+    mem_cap: int = 0
+    mem_dt: float = 0.0
+    mem_tmax: float = 0.0
+    mem_pen: float = 0.0
 
     def c(self) -> lmx_params:
         return lmx_params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1, self.lambda2,
-                          self.tau, self.slo_mult, self.slo_const, self.sigma_floor, self.lc0, self.alpha)
+                          self.tau, self.slo_mult, self.slo_const, self.sigma_floor, self.lc0, self.alpha,
+                          self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax, self.mem_pen)
 
 
 class Context:

@@ -6,7 +6,8 @@ import numpy as np
 import oracle
 import workload
 
-INT_FIELDS = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version", "status")
+INT_FIELDS = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version", "status",
+              "n_mem_wait", "n_offload")
 F64_FIELDS = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util", "mean_len_std")
 REL_TOL = 1e-12   # north_star: fp summaries within 1e-12 relative
 
@@ -15,7 +16,8 @@ def oracle_params(lp) -> oracle.OracleParams:
     return oracle.OracleParams(policy=lp.policy, lambda1=lp.lambda1, lambda2=lp.lambda2, tau=lp.tau,
                                slo_mult=lp.slo_mult, sigma_floor=lp.sigma_floor, lc0=lp.lc0, alpha=lp.alpha,
                                deprioritize=lp.deprioritize, slo_mode=lp.slo_mode, qcap=lp.qcap,
-                               slo_const=lp.slo_const)
+                               slo_const=lp.slo_const, mem_enable=lp.mem_enable, mem_cap=lp.mem_cap,
+                               mem_dt=lp.mem_dt, mem_tmax=lp.mem_tmax, mem_pen=lp.mem_pen)
 
 
 def rel_err(a, b):
