@@ -117,7 +117,19 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def oracle_sample(traces, n_threads, policy=0):
+# Algorithm 2 variant (--mem-cap > 0): Llama-8B stage reference forward 0.055 s
+# -> T_max = 10x, Delta_t = 0.1x; offload penalty 2.2 MB/token of
+# activations over a ~25 GB/s host link = 8.8e-5 s/token (DESIGN.md R-mem)
+MEM_DT, MEM_TMAX, MEM_PEN = 0.0055, 0.55, 8.8e-5
+
+
+def mem_kw(args):
+    if not getattr(args, "mem_cap", 0):
+        return {}
+    return dict(mem_enable=1, mem_cap=int(args.mem_cap), mem_dt=MEM_DT, mem_tmax=MEM_TMAX, mem_pen=MEM_PEN)
+
+
+def oracle_sample(traces, n_threads, policy=0, mem=None):
     """Run the oracle as it stands over a trace batch, threads over slices."""
     import concurrent.futures as cf
 
@@ -130,7 +142,8 @@ def oracle_sample(traces, n_threads, policy=0):
 
     def work(b):
         sub = traces.subset(range(b[0], b[1]))
-        return oracle.run_batch(ef, eb, N_NODES, N_STAGES, sub, oracle.OracleParams(policy=policy), outputs=False)
+        return oracle.run_batch(ef, eb, N_NODES, N_STAGES, sub, oracle.OracleParams(policy=policy, **(mem or {})),
+                                outputs=False)
 
     t0 = time.perf_counter()
     with cf.ThreadPoolExecutor(len(bounds)) as ex:
@@ -155,9 +168,11 @@ def config_dict(args, world):
     return {"workload": (f"mc: {args.traces} seeded traces/GPU x {args.n_inf} inference requests + "
                          f"{args.n_train} training micro-batches (half Poisson, half bursty CV=3), "
                          f"LogNormal lengths, N={N_NODES} nodes x S={N_STAGES} stages, Llama-8B profile, "
-                         f"LeMix, summary-only"),
+                         f"LeMix, summary-only"
+                         + (f", Algorithm 2 memory model (cap {args.mem_cap} tokens/GPU, dt {MEM_DT} s, "
+                            f"T_max {MEM_TMAX} s)" if args.mem_cap else "")),
             "traces_per_gpu": args.traces, "tasks_per_trace": per, "n_nodes": N_NODES, "n_stages": N_STAGES,
-            "policy": "lemix", "qcap": args.qcap,
+            "policy": "lemix", "qcap": args.qcap, "mem_cap_tokens": args.mem_cap or None,
             "l2": f"inputs {args.traces * per * 12 / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)",
             "parallelism": f"dp{world} (independent traces sharded, one NCCL summary all-reduce)"}
 
@@ -178,7 +193,7 @@ def run_reference(args, rank, world):
     threads = os.cpu_count() or 1
     times = []
     for k in range(args.warmup + args.steps):
-        _, counters, dt, used = oracle_sample(tr, threads)
+        _, counters, dt, used = oracle_sample(tr, threads, mem=mem_kw(args))
         if k >= args.warmup:
             times.append(dt)
     decisions = tr.n_tasks
@@ -211,6 +226,8 @@ def main():
     ap.add_argument("--check-traces", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--mem-cap", type=int, default=0,
+                    help="> 0: run Algorithm 2 (memory-aware execution) with this many activation tokens per GPU")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -258,7 +275,7 @@ def main():
     torch.cuda.synchronize()
 
     ef, eb = workload.profile(N_NODES, N_STAGES)
-    params = lemix.Params(policy=lemix.LMX_LEMIX, qcap=args.qcap)
+    params = lemix.Params(policy=lemix.LMX_LEMIX, qcap=args.qcap, **mem_kw(args))
     ctx = lemix.Context(local_rank, stream.cuda_stream)
     ctx.lmx_load_profile(N_NODES, N_STAGES, ef, eb)
     ctx.lmx_load_traces(tr.offsets, tr.n_inf, arrival_d, lbk_d, mem=lemix.LMX_DEVICE)
@@ -359,7 +376,7 @@ def main():
         n_cpu = min(n_cpu, T)
         idx = sample_indices(T, n_cpu)
         sub = tr.subset(idx)
-        osum, counters, dt, used = oracle_sample(sub, threads)
+        osum, counters, dt, used = oracle_sample(sub, threads, mem=mem_kw(args))
         # sampled parity in the bench's own launch configuration (summary-only run)
         gs = sums_gpu[idx]
         same_int = all(np.array_equal(gs[k], osum[k]) for k in lemix.SUMMARY_INT)
@@ -386,7 +403,7 @@ def main():
             pass
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                     "frac": achieved / peak_tflops, "traffic": traffic,
-                    "kernel": "lmx::event_loop_kernel<2,1>",
+                    "kernel": f"lmx::tile::event_loop_kernel<2, true, 1, true, 4, {str(bool(args.mem_cap)).lower()}>",
                     "note": (f"fp64 pipe: {opd:.1f} algorithmic fp64 ops/decision (oracle counters x DESIGN.md "
                              f"weights) x {M} decisions / {k_s * 1e3:.1f} ms mean kernel time; peak = 64 "
                              f"DP lanes/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz ({peak_src} clock); "
