@@ -112,15 +112,18 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S) * cstride; };
     auto c_sl2 = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S + 1) * cstride; };
     auto c_ntr = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S + 2) * cstride; };
+    // rarely used per-trace words (same column layout, after the node slots):
+    // 0 trace index, 1 first task offset, 2 t_first, 3 error (task << 8 | field)
+    auto c_tw = [&](int k) { return cbase + (uint32_t)(NPL * (2 * S + 3) + k) * cstride; };
 
     // ---- per-trace (tile-replicated) state ----
     bool active = false, finished = false;
-    long long t = 0, o = 0;
+    long long t = 0;                      // (claim only; kept in c_tw(0) across the trace)
     const double *tarr = p.arrival;      // this trace's task arrays (32-bit indexing)
     const uint32_t *tlbk = p.lbk;
     int nI = 0, nT = 0, i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0;
-    int cur_defer = 0, status = LMX_OK, err_task = 0, err_code = kErrNone;
-    double r = kInf, t_first = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
+    int cur_defer = 0, status = LMX_OK;
+    double r = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
     long long n_slo = 0, sum_ver = 0, n_def = 0;
     int n_mwait = 0, n_moff = 0;          // Algorithm 2 counters (MEM)
     double a_inf = 0.0, a_inf2 = 0.0, a_tr = 0.0, a_tr2 = 0.0;   // 2-deep input prefetch
@@ -144,7 +147,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 finished = true;
             } else {
                 t = (long long)tt;
-                o = p.offsets[t];
+                const long long o = p.offsets[t];
                 const int len = (int)(p.offsets[t + 1] - o);
                 dev::wait_inputs(p.ready, p.chunk_tasks, o, o + len);
                 nI = p.n_inf[t];
@@ -153,8 +156,9 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 tlbk = p.lbk + o;
                 i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
                 status = LMX_OK;
-                err_task = 0;
-                err_code = kErrNone;
+                dev::sts_l(c_tw(0), t);
+                dev::sts_l(c_tw(1), o);
+                dev::sts_l(c_tw(3), kErrNone);
                 n_slo = sum_ver = n_def = 0;
                 n_mwait = n_moff = 0;
                 sum_ttft = 0.0;
@@ -165,9 +169,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 if (nT > 0) { a_tr = __ldg(tarr + nI); v_tr = __ldg(tlbk + nI); }
                 if (nT > 1) { a_tr2 = __ldg(tarr + nI + 1); v_tr2 = __ldg(tlbk + nI + 1); }
                 r = (nT > 0) ? a_tr : kInf;
-                t_first = kInf;
+                double t_first = kInf;
                 if (nI > 0) t_first = dev::dmin(t_first, a_inf);
                 if (nT > 0) t_first = dev::dmin(t_first, a_tr);
+                dev::sts_d(c_tw(2), t_first);
 #pragma unroll
                 for (int jj = 0; jj < NPL; ++jj) {
                     hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = 0;
@@ -187,7 +192,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 }
                 if (!LEMIX && p.policy == LMX_SEPARATE && N == 1 && nI > 0 && nT > 0) {
                     status = LMX_EINVAL;
-                    err_code = kErrSeparateN1;
+                    dev::sts_l(c_tw(3), kErrSeparateN1);
                 }
                 active = true;
             }
@@ -218,7 +223,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 sm.n_mem_wait = n_mwait;
                 sm.n_offload = n_moff;
                 sm.sum_ttft = sum_ttft;
-                sm.makespan = (ntask > 0) ? t_last - t_first : 0.0;
+                sm.makespan = (ntask > 0) ? t_last - dev::lds_d(c_tw(2)) : 0.0;
                 sm.throughput = (sm.makespan > 0.0) ? (double)ntask / sm.makespan : 0.0;
                 sm.mean_ttft = (nI > 0) ? sum_ttft / (double)nI : 0.0;
                 sm.slo_attainment = (nI > 0) ? (double)n_slo / (double)nI : 1.0;
@@ -258,10 +263,11 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 sm.mean_len_std = (act > 0) ? stds / (double)act : 0.0;
             }
             if (tl == 0) {
-                p.summaries[t] = sm;
+                const long long tt = dev::lds_l(c_tw(0));
+                p.summaries[tt] = sm;
                 if (status != LMX_OK) {
-                    p.trace_err[t] = ((long long)err_task << 8) | err_code;
-                    atomicMin(p.first_bad, (unsigned long long)t);
+                    p.trace_err[tt] = dev::lds_l(c_tw(3));
+                    atomicMin(p.first_bad, (unsigned long long)tt);
                 }
             }
             active = false;
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                           (is_train | (arr >= a_last_inf));
                 int fx = 0;
                 if (!LEMIX && p.policy == LMX_FIXED) {
-                    fx = __ldg(p.fixed + o + task);
+                    fx = __ldg(p.fixed + dev::lds_l(c_tw(1)) + task);
                     ok = ok & (fx >= 0) & (fx < N);
                 }
                 if (!ok) {
@@ -327,8 +333,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     else if (!(arr >= 0.0 && arr < kInf)) code = kErrArrival;
                     else if (!is_train && arr < a_last_inf) code = kErrOrder;
                     status = LMX_EINVAL;
-                    err_task = task;
-                    err_code = code;
+                    dev::sts_l(c_tw(3), ((long long)task << 8) | code);
                 }
             }
             if (!deferred && status == LMX_OK) {
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         chosen = sep_i++ % (N - p.n_tr_sep);
                     }
                 } else {
-                    chosen = __ldg(p.fixed + o + task);
+                    chosen = __ldg(p.fixed + dev::lds_l(c_tw(1)) + task);
                 }
 
                 // ---- a3-a7: Algorithm 1 + Eq. 1-3 for every candidate this lane owns ----
@@ -544,6 +549,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 } else {
                     // ---- a11: outputs + per-trace folds ----
                     if (tl == 0 && p.node_defer) {
+                        const long long o = dev::lds_l(c_tw(1));
                         const unsigned dsat = is_train ? (unsigned)min(cur_defer, 0xFFFF) : 0u;
                         p.node_defer[o + task] = (uint32_t)best | (dsat << 16);
                         p.decision_idx[o + task] = step;
