@@ -47,7 +47,7 @@ inline int stages_bucket(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : 
 inline int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
 inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN : 0; }
 // 8-byte shared-memory words of commit-only state per node slot and thread
-inline int cold_words(int S) { return 2 * S + 3; }
+__host__ __device__ inline int cold_words(int S) { return 2 * S + 7; }
 
 template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, bool MEM>
 __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
@@ -105,16 +105,21 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     // LB[s] (last planned backward end), busy[s], sum l, sum l^2, and
     // (training count, version pointer) -- see cold_words()
     const uint32_t cstride = 8u * blockDim.x;
+    const int CW = cold_words(S);          // words per node slot
+    constexpr bool SCOLD = NPL > 1;
     const uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
                            (uint32_t)(W > 0 ? NPL * W * ring_words(S, MEM) : 0) * wstride + 8u * threadIdx.x;
-    auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + s) * cstride; };
-    auto c_busy = [&](int jj, int s) { return cbase + (uint32_t)(jj * (2 * S + 3) + S + s) * cstride; };
-    auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S) * cstride; };
-    auto c_sl2 = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S + 1) * cstride; };
-    auto c_ntr = [&](int jj) { return cbase + (uint32_t)(jj * (2 * S + 3) + 2 * S + 2) * cstride; };
+    auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * CW + s) * cstride; };
+    auto c_busy = [&](int jj, int s) { return cbase + (uint32_t)(jj * CW + S + s) * cstride; };
+    auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S) * cstride; };
+    auto c_sl2 = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 1) * cstride; };
+    auto c_ntr = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 2) * cstride; };
     // rarely used per-trace words (same column layout, after the node slots):
     // 0 trace index, 1 first task offset, 2 t_first, 3 error (task << 8 | field)
-    auto c_tw = [&](int k) { return cbase + (uint32_t)(NPL * (2 * S + 3) + k) * cstride; };
+    auto c_tw = [&](int k) { return cbase + (uint32_t)(NPL * CW + k) * cstride; };
+    // SCOLD (several nodes per lane): a_[-1], mu, 1/(2 sigma^2), 1/(sigma sqrt(2 pi))
+    // of each node also live in shared memory (read once per decision)
+    auto c_sc = [&](int jj, int f) { return cbase + (uint32_t)(jj * CW + 2 * S + 3 + f) * cstride; };
 
     // ---- per-trace (tile-replicated) state ----
     bool active = false, finished = false;
@@ -177,6 +182,9 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 for (int jj = 0; jj < NPL; ++jj) {
                     hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = 0;
                     aprev[jj] = mu[jj] = kk[jj] = cc[jj] = 0.0;
+                    if (SCOLD)
+#pragma unroll
+                        for (int f = 0; f < 4; ++f) dev::sts_d(c_sc(jj, f), 0.0);
                     dev::sts_l(c_sl(jj), 0);
                     dev::sts_l(c_sl2(jj), 0);
                     dev::sts_l(c_ntr(jj), 0);      // training count | version pointer << 32
@@ -384,8 +392,11 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         // nodes too and discarded (its value is finite for t >= 0)
                         double LC = p.lc0;
                         if (LEMIX) {
-                            const double d = (double)l - mu[jj];
-                            const double lw = cc[jj] * dev::exp_neg((d * d) * kk[jj]);
+                            const double mu_j = SCOLD ? dev::lds_d(c_sc(jj, 1)) : mu[jj];
+                            const double kk_j = SCOLD ? dev::lds_d(c_sc(jj, 2)) : kk[jj];
+                            const double cc_j = SCOLD ? dev::lds_d(c_sc(jj, 3)) : cc[jj];
+                            const double d = (double)l - mu_j;
+                            const double lw = cc_j * dev::exp_neg((d * d) * kk_j);
                             LC = (cnt[jj] < 2) ? p.lc0 : lw;
                         }
                         double II;
@@ -400,7 +411,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         qn[jj] = qlen - gc;
                         if (LEMIX) {
                             const double R = dev::last_of(en_s[jj], S) - a;               // line 20
-                            const double a_last = hasp[jj] ? aprev[jj] : a;               // R-9
+                            const double ap_j = SCOLD ? dev::lds_d(c_sc(jj, 0)) : aprev[jj];
+                            const double a_last = hasp[jj] ? ap_j : a;                   // R-9
                             const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
                             const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
                             const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
@@ -477,7 +489,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                             const long long trv = dev::lds_l(c_ntr(jj));
                             int ntr = (int)(trv & 0xffffffffll), vp = (int)(trv >> 32);
                             hasp[jj] = 1;
-                            aprev[jj] = a;
+                            if (SCOLD) dev::sts_d(c_sc(jj, 0), a); else aprev[jj] = a;
                             c_en0 = en_s[jj][0];
                             c_st0 = st0_s[jj];
                             c_done = dev::last_of(en_s[jj], S);
@@ -528,9 +540,15 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                                 cnt[jj]++;
                                 dev::sts_l(c_sl(jj), sl_n[jj]);
                                 dev::sts_l(c_sl2(jj), sl2_n[jj]);
-                                mu[jj] = mu_n[jj];
-                                kk[jj] = kk_n[jj];
-                                cc[jj] = cc_n[jj];
+                                if (SCOLD) {
+                                    dev::sts_d(c_sc(jj, 1), mu_n[jj]);
+                                    dev::sts_d(c_sc(jj, 2), kk_n[jj]);
+                                    dev::sts_d(c_sc(jj, 3), cc_n[jj]);
+                                } else {
+                                    mu[jj] = mu_n[jj];
+                                    kk[jj] = kk_n[jj];
+                                    cc[jj] = cc_n[jj];
+                                }
                             }
                         }
                     }
