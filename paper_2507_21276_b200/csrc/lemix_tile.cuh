@@ -30,6 +30,9 @@
 #ifndef LMX_TILE_WIN
 #define LMX_TILE_WIN 4                      // ring tail-window entries in shared memory (S <= 2)
 #endif
+#ifndef LMX_TILE_L1PF
+#define LMX_TILE_L1PF 0                     // L1 prefetch of the next inputs at decision start (measured slower)
+#endif
 #ifndef LMX_TILE_MINB
 #define LMX_TILE_MINB 4                     // resident CTAs/SM the register budget targets
 #endif
@@ -281,6 +284,15 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
             active = false;
         } else {
             // ---- a1: event selection (ties -> inference) ----
+#if LMX_TILE_L1PF
+            // Pull the inputs the end-of-decision loads will read (two ahead in
+            // each stream) into L1 now, without occupying registers, so those
+            // loads -- which the next iteration's control flow waits on -- hit L1.
+            dev::prefetch_l1(tarr + min(i + 2, nI - 1));
+            dev::prefetch_l1(tlbk + min(i + 2, nI - 1));
+            dev::prefetch_l1(tarr + nI + min(j + 2, nT - 1));
+            dev::prefetch_l1(tlbk + nI + min(j + 2, nT - 1));
+#endif
             const double t_inf = (i < nI) ? a_inf : kInf;
             const bool is_train = !(t_inf <= r);
             const double now = is_train ? r : t_inf;
