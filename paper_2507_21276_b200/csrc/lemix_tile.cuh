@@ -50,7 +50,8 @@ inline int stages_bucket(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : 
 inline int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
 inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN : 0; }
 // 8-byte shared-memory words of commit-only state per node slot and thread
-__host__ __device__ inline int cold_words(int S) { return 2 * S + 7; }
+// (+ 4 words of scoring state when a lane owns several nodes, see SCOLD)
+__host__ __device__ inline int cold_words(int S, bool scold) { return 2 * S + 3 + (scold ? 4 : 0); }
 
 template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, bool MEM>
 __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
@@ -108,8 +109,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     // LB[s] (last planned backward end), busy[s], sum l, sum l^2, and
     // (training count, version pointer) -- see cold_words()
     const uint32_t cstride = 8u * blockDim.x;
-    const int CW = cold_words(S);          // words per node slot
     constexpr bool SCOLD = NPL > 1;
+    const int CW = cold_words(S, SCOLD);   // words per node slot
     const uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
                            (uint32_t)(W > 0 ? NPL * W * ring_words(S, MEM) : 0) * wstride + 8u * threadIdx.x;
     auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * CW + s) * cstride; };
