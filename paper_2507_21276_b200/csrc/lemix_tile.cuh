@@ -209,12 +209,15 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 active = true;
             }
         }
-        if (!active) continue;   // (finished lanes only: back to the warp vote)
-
-        const bool more = (i < nI) | (j < nT);
+        // Tiles without a trace (finished) stay in the loop as passengers
+        // (live = false): every lane of the warp then reaches the full-warp
+        // shuffles of the decision below together, so they need no
+        // divergence-tolerant mask handling.
+        const bool more = active & ((i < nI) | (j < nT));
         iters += more;
         if (more & (iters > 2 * (nI + nT) + 2)) status = LMX_EBUDGET;
-        const bool done_trace = (status != LMX_OK) | !more;
+        const bool done_trace = active & ((status != LMX_OK) | !more);
+        const bool live = active & !done_trace;
 
         if (done_trace) {
             // ---- per-trace metrics, node folds in node order ----
@@ -283,7 +286,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 }
             }
             active = false;
-        } else {
+        }
+        {
             // ---- a1: event selection (ties -> inference) ----
 #if LMX_TILE_L1PF
             // Pull the inputs the end-of-decision loads will read (two ahead in
@@ -299,9 +303,11 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
             const double now = is_train ? r : t_inf;
             const uint32_t v = is_train ? v_tr : v_inf;
             bool deferred = false;
-            if (LEMIX && is_train && p.deprioritize && i < nI) {
+            if (LEMIX) {
                 // ---- a2: Eq. 4 queue-level deprioritisation against the next
-                // enqueued inference task (R-14/R-15) ----
+                // enqueued inference task (R-14/R-15);
+                // the tile min is formed by every lane, used where it applies ----
+                const bool eq4 = live && is_train && p.deprioritize && i < nI;
                 const double wn = task_w(v_inf);
                 double m = kInf;
 #pragma unroll
@@ -313,7 +319,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     }
                 }
                 #pragma unroll
-                for (int off = T >> 1; off > 0; off >>= 1) m = dev::dmin(m, dev::shfl_xor_d(tmask, m, off));
+                for (int off = T >> 1; off > 0; off >>= 1) m = dev::dmin(m, dev::shfl_xor_w(m, off, T));
+                if (eq4) {
                 double tauR;
                 if (p.slo_mode == 1) {
                     tauR = p.slo_const;
@@ -330,9 +337,10 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     cur_defer++;
                     n_def++;
                 }
+                }
             }
             const int task = is_train ? nI + j : i;
-            if (!deferred) {
+            if (live && !deferred) {
                 // ---- input validation of the task being placed (one predicate;
                 // the error code is worked out only on the rare failure path) ----
                 const double arr = is_train ? a_tr : a_inf;
@@ -357,14 +365,15 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     dev::sts_l(c_tw(3), ((long long)task << 8) | code);
                 }
             }
-            if (!deferred && status == LMX_OK) {
+            const bool place = live && !deferred && status == LMX_OK;   // this tile places a task
+            {
                 const double a = now;                    // dispatch time (R-2)
                 const double w = task_w(v);
                 const int l = task_len(v);
 
                 // ---- a9: baseline selectors ----
                 int chosen = -1;
-                if (LEMIX) {
+                if (LEMIX || !place) {
                 } else if (p.policy == LMX_RR) {
                     chosen = rr % N;
                     rr++;
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     for (int s = 0; s < SMAX; ++s) en_s[jj][s] = 0.0;
                     mu_n[jj] = kk_n[jj] = cc_n[jj] = 0.0;
                     sl_n[jj] = sl2_n[jj] = 0;
-                    if (n < N && (LEMIX || n == chosen)) {
+                    if (place && n < N && (LEMIX || n == chosen)) {
                         // Eq. 2 of this candidate, ahead of (and
                         // independent of) Algorithm 1; exp_neg is evaluated for cold
                         // nodes too and discarded (its value is finite for t >= 0)
@@ -453,8 +462,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                 if (LEMIX) {
 #pragma unroll
                     for (int off = T >> 1; off > 0; off >>= 1) {
-                        const double f2 = dev::shfl_xor_d(tmask, f_best, off);
-                        const int n2 = __shfl_xor_sync(tmask, n_best, off);
+                        const double f2 = dev::shfl_xor_w(f_best, off, T);
+                        const int n2 = __shfl_xor_sync(0xffffffffu, n_best, off, T);
                         if (n2 != INT_MAX &&
                             (n_best == INT_MAX || f2 > f_best || (f2 == f_best && n2 < n_best))) {
                             f_best = f2;
@@ -468,10 +477,11 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
 
                 // ---- a10: commit on the owning lane ----
                 const int owner = tbase + (best & (T - 1));
+                const int osrc = best & (T - 1);        // owner within the tile
                 const int jb = best >> log2T;
                 double c_done = 0.0, c_en0 = 0.0, c_st0 = 0.0;
                 int c_ver = 0, c_status = LMX_OK, c_mem = 0;
-                if (lane == owner) {
+                if (place && lane == owner) {
 #pragma unroll
                     for (int jj = 0; jj < NPL; ++jj) {
                         if (jj == jb) {
@@ -567,15 +577,16 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     }
                 }
                 if (c_status != LMX_OK) c_ver = INT_MIN;   // (a version count is never negative)
-                c_done = dev::shfl_d(tmask, c_done, owner);
-                c_en0 = dev::shfl_d(tmask, c_en0, owner);
-                if (p.node_defer) c_st0 = dev::shfl_d(tmask, c_st0, owner);
-                c_ver = __shfl_sync(tmask, c_ver, owner);
+                c_done = dev::shfl_w(c_done, osrc, T);
+                c_en0 = dev::shfl_w(c_en0, osrc, T);
+                if (p.node_defer) c_st0 = dev::shfl_w(c_st0, osrc, T);
+                c_ver = __shfl_sync(0xffffffffu, c_ver, osrc, T);
                 if (MEM) {
-                    c_mem = __shfl_sync(tmask, c_mem, owner);
-                    if (c_ver != INT_MIN) { n_mwait += c_mem & 0xff; n_moff += c_mem >> 8; }
+                    c_mem = __shfl_sync(0xffffffffu, c_mem, osrc, T);
+                    if (place && c_ver != INT_MIN) { n_mwait += c_mem & 0xff; n_moff += c_mem >> 8; }
                 }
-                if (c_ver == INT_MIN) {
+                if (!place) {
+                } else if (c_ver == INT_MIN) {
                     status = LMX_EQCAP;
                 } else {
                     // ---- a11: outputs + per-trace folds ----
