@@ -241,7 +241,10 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             double II;
                             int gc;
                             const dev::Ring q{ring_be + (rb0 + n * K) * ring_words(S), p.kmask, S, 0u, 0u, qh[n] + qn[n]};
-                            dev::plan<SMAX, LMX_LANE_PF>(P[n], (hasp >> n) & 1u, S, s_ef + n * S, s_eb + n * S, q, qh[n], qn[n],
+                            double efn[SMAX], ebn[SMAX];
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s) { efn[s] = (s < S) ? s_ef[n * S + s] : 0.0; ebn[s] = (s < S) ? s_eb[n * S + s] : 0.0; }
+                            dev::plan<SMAX, LMX_LANE_PF>(P[n], (hasp >> n) & 1u, S, efn, ebn, q, qh[n], qn[n],
                                             sk, w, a, now, en[n], st0[n], II, gc);
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
@@ -307,7 +310,10 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     double II;
                     int gc;
                     const dev::Ring q{ring_be + (rb0 + best * K) * ring_words(S), p.kmask, S, 0u, 0u, qhc + qnc};
-                    dev::plan<SMAX, LMX_LANE_PF>(Pc, (hasp >> best) & 1u, S, s_ef + best * S, s_eb + best * S, q, qhc, qnc, sk,
+                    double efb[SMAX], ebb[SMAX];
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) { efb[s] = (s < S) ? s_ef[best * S + s] : 0.0; ebb[s] = (s < S) ? s_eb[best * S + s] : 0.0; }
+                    dev::plan<SMAX, LMX_LANE_PF>(Pc, (hasp >> best) & 1u, S, efb, ebb, q, qhc, qnc, sk,
                                     w, a, now, en_b, st0_b, II, gc);
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s)

@@ -75,11 +75,12 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     }
     __syncthreads();
     dev::mbar_wait(&s_bar, 0);
-    const double *s_ef = s_eta;
-    const double *s_eb = s_eta + NS;
+    uint32_t s_eta_u = dev::smem_u32(s_eta);
+    dev::opaque(s_eta_u);
+    const dev::SmemProfile prof{s_eta_u, NS, S};
     double ef0[SMAX];   // eta_F of node 0, for tau_R (R-16)
 #pragma unroll
-    for (int s = 0; s < SMAX; ++s) ef0[s] = (s < S) ? s_ef[s] : 0.0;
+    for (int s = 0; s < SMAX; ++s) ef0[s] = (s < S) ? prof.f(0, s) : 0.0;
 
     // ---- tile geometry ----
     const int lane = threadIdx.x & 31;
@@ -101,6 +102,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     for (int jj = 0; jj < NPL; ++jj) {
         ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * ring_words(S, MEM)) * wstride +
                  16u * threadIdx.x;
+        dev::opaque(ws[jj]);   // keep in a register: no per-iteration rematerialisation
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
         rbe[jj] = p.ring_be + rbase * ring_words(S, MEM);
     }
@@ -111,8 +113,9 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     const uint32_t cstride = 8u * blockDim.x;
     constexpr bool SCOLD = NPL > 1;
     const int CW = cold_words(S, SCOLD);   // words per node slot
-    const uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
-                           (uint32_t)(W > 0 ? NPL * W * ring_words(S, MEM) : 0) * wstride + 8u * threadIdx.x;
+    uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
+                     (uint32_t)(W > 0 ? NPL * W * ring_words(S, MEM) : 0) * wstride + 8u * threadIdx.x;
+    dev::opaque(cbase);
     auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * CW + s) * cstride; };
     auto c_busy = [&](int jj, int s) { return cbase + (uint32_t)(jj * CW + S + s) * cstride; };
     auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S) * cstride; };
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     const int n = tl + jj * T;
                     if (n < N) {
                         const double latest = hasp[jj] ? dev::last_of(P[jj], S) : -kInf;
-                        m = dev::dmin(m, latest + s_ef[n * S + S - 1] * wn);
+                        m = dev::dmin(m, latest + prof.f(n, S - 1) * wn);
                     }
                 }
                 #pragma unroll
@@ -425,7 +428,9 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         int gc;
                         const int qhead = qh[jj], qlen = qn[jj];
                         const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
-                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, s_ef + n * S, s_eb + n * S, q, qhead, qlen, sk[jj], w,
+                        double efn[SMAX], ebn[SMAX];
+                        prof.node<SMAX>(n, efn, ebn);
+                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, efn, ebn, q, qhead, qlen, sk[jj], w,
                                         a, now, en_s[jj], st0_s[jj], II, gc);
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
                         // end_b^1 is non-decreasing along the queue)
@@ -485,8 +490,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
 #pragma unroll
                     for (int jj = 0; jj < NPL; ++jj) {
                         if (jj == jb) {
-                            const double *ef = s_ef + best * S;
-                            const double *eb = s_eb + best * S;
+                            double ef[SMAX], eb[SMAX];
+                            prof.node<SMAX>(best, ef, eb);
                             const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
                             const long long tok = (long long)task_batch(v) * l;   // activation tokens C*l
                             int offm = 0;
