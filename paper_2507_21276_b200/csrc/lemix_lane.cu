@@ -244,8 +244,12 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                             double efn[SMAX], ebn[SMAX];
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s) { efn[s] = (s < S) ? s_ef[n * S + s] : 0.0; ebn[s] = (s < S) ? s_eb[n * S + s] : 0.0; }
+                            double skeb[SMAX];   // (no cache here: read the last stale entry)
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                skeb[s] = (s < S && sk[s] > qh[n]) ? q.at(sk[s] - 1, s).y : 0.0;
                             dev::plan<SMAX, LMX_LANE_PF>(P[n], (hasp >> n) & 1u, S, efn, ebn, q, qh[n], qn[n],
-                                            sk, w, a, now, en[n], st0[n], II, gc);
+                                            sk, skeb, w, a, now, en[n], st0[n], II, gc);
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
                                 if (s < S) SK_(n, s) = sk[s];
@@ -313,8 +317,11 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     double efb[SMAX], ebb[SMAX];
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s) { efb[s] = (s < S) ? s_ef[best * S + s] : 0.0; ebb[s] = (s < S) ? s_eb[best * S + s] : 0.0; }
+                    double skeb[SMAX];
+#pragma unroll
+                    for (int s = 0; s < SMAX; ++s) skeb[s] = (s < S && sk[s] > qhc) ? q.at(sk[s] - 1, s).y : 0.0;
                     dev::plan<SMAX, LMX_LANE_PF>(Pc, (hasp >> best) & 1u, S, efb, ebb, q, qhc, qnc, sk,
-                                    w, a, now, en_b, st0_b, II, gc);
+                                    skeb, w, a, now, en_b, st0_b, II, gc);
 #pragma unroll
                     for (int s = 0; s < SMAX; ++s)
                         if (s < S) SK_(best, s) = sk[s];

@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
     double aprev[NPL], mu[NPL], kk[NPL], cc[NPL];
     int hasp[NPL], qh[NPL], qn[NPL], cnt[NPL];
     int sk[NPL][SMAX];   // stale-prefix pointers (see dev::plan)
+    double skeb[NPL][SMAX];   // end_b^s of the last stale entry (see dev::plan)
 
     // Control flow inside the loop is structured (no continue/break out of a
     // branch) so tiles that took different branches reconverge right after it.
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     for (int s = 0; s < SMAX; ++s) {
                         P[jj][s] = 0.0;
                         sk[jj][s] = 0;
+                        skeb[jj][s] = 0.0;
                         if (s < S) {
                             dev::sts_d(c_lb(jj, s), -kInf);
                             dev::sts_d(c_busy(jj, s), 0.0);
@@ -430,7 +432,7 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
                         double efn[SMAX], ebn[SMAX];
                         prof.node<SMAX>(n, efn, ebn);
-                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, efn, ebn, q, qhead, qlen, sk[jj], w,
+                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, efn, ebn, q, qhead, qlen, sk[jj], skeb[jj], w,
                                         a, now, en_s[jj], st0_s[jj], II, gc);
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
                         // end_b^1 is non-decreasing along the queue)
