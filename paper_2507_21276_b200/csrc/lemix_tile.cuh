@@ -307,6 +307,14 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
             const bool is_train = !(t_inf <= r);
             const double now = is_train ? r : t_inf;
             const uint32_t v = is_train ? v_tr : v_inf;
+            // Inputs two ahead in the stream this decision consumes, loaded
+            // now so they land while the decision runs (loaded at its end, the
+            // loop-carried register copies at the top of the next iteration
+            // would wait for them).  Discarded when the task is deferred.
+            const bool pf_ok = live && (is_train ? nT > 0 : nI > 0);
+            const int pf_idx = is_train ? nI + min(j + 2, nT - 1) : min(i + 2, nI - 1);
+            const double pf_a = pf_ok ? __ldg(tarr + pf_idx) : 0.0;
+            const uint32_t pf_v = pf_ok ? __ldg(tlbk + pf_idx) : 0u;
             bool deferred = false;
             if (LEMIX) {
                 // ---- a2: Eq. 4 queue-level deprioritisation against the next
@@ -612,11 +620,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         cur_defer = 0;
                         a_tr = a_tr2;
                         v_tr = v_tr2;
-                        {   // prefetch two ahead (clamped index: no branch)
-                            const int jn = min(j + 1, nT - 1);
-                            a_tr2 = __ldg(tarr + nI + jn);
-                            v_tr2 = __ldg(tlbk + nI + jn);
-                        }
+                        a_tr2 = pf_a;          // task min(j + 1, nT - 1), loaded above
+                        v_tr2 = pf_v;
                         // next release: max(a_min, this task's S1 forward end)
                         r = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
                     } else {
@@ -638,11 +643,8 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                         i++;
                         a_inf = a_inf2;
                         v_inf = v_inf2;
-                        {   // prefetch two ahead (clamped index: no branch)
-                            const int in2 = min(i + 1, nI - 1);
-                            a_inf2 = __ldg(tarr + in2);
-                            v_inf2 = __ldg(tlbk + in2);
-                        }
+                        a_inf2 = pf_a;         // task min(i + 1, nI - 1), loaded above
+                        v_inf2 = pf_v;
                     }
                 }
             }
