@@ -615,37 +615,40 @@ __global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const
                     }
                     t_last = dev::dmax(t_last, c_done);
                     step++;
-                    if (is_train) {
-                        j++;
-                        cur_defer = 0;
-                        a_tr = a_tr2;
-                        v_tr = v_tr2;
-                        a_tr2 = pf_a;          // task min(j + 1, nT - 1), loaded above
-                        v_tr2 = pf_v;
-                        // next release: max(a_min, this task's S1 forward end)
-                        r = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
+                    // both kinds' folds as selects (no divergence between tiles
+                    // that placed a training and an inference task)
+                    const bool inf = !is_train;
+                    const double ttft = c_done - a;            // R from arrival
+                    double tauR;
+                    if (p.slo_mode == 1) {
+                        tauR = p.slo_const;
                     } else {
-                        const double ttft = c_done - a;        // R from arrival
-                        sum_ttft = sum_ttft + ttft;
-                        double tauR;
-                        if (p.slo_mode == 1) {
-                            tauR = p.slo_const;
-                        } else {
-                            double acc = 0.0;
+                        double acc = 0.0;
 #pragma unroll
-                            for (int s = 0; s < SMAX; ++s)
-                                if (s < S) acc = acc + ef0[s] * w;
-                            tauR = p.slo_mult * acc;
-                        }
-                        if (ttft <= tauR) n_slo++;          // SLO: TTFT <= 5x forward latency
-                        sum_ver += c_ver;
-                        a_last_inf = a;
-                        i++;
-                        a_inf = a_inf2;
-                        v_inf = v_inf2;
-                        a_inf2 = pf_a;         // task min(i + 1, nI - 1), loaded above
-                        v_inf2 = pf_v;
+                        for (int s = 0; s < SMAX; ++s)
+                            if (s < S) acc = acc + ef0[s] * w;
+                        tauR = p.slo_mult * acc;
                     }
+                    const double sum_ttft_n = sum_ttft + ttft;
+                    sum_ttft = inf ? sum_ttft_n : sum_ttft;
+                    n_slo += (inf && ttft <= tauR) ? 1 : 0;   // SLO: TTFT <= 5x forward latency
+                    sum_ver += inf ? c_ver : 0;
+                    a_last_inf = inf ? a : a_last_inf;
+                    i += inf ? 1 : 0;
+                    j += inf ? 0 : 1;
+                    cur_defer = inf ? cur_defer : 0;
+                    // the consumed stream advances; its task two ahead was loaded above
+                    a_inf = inf ? a_inf2 : a_inf;
+                    v_inf = inf ? v_inf2 : v_inf;
+                    a_inf2 = inf ? pf_a : a_inf2;
+                    v_inf2 = inf ? pf_v : v_inf2;
+                    a_tr = inf ? a_tr : a_tr2;
+                    v_tr = inf ? v_tr : v_tr2;
+                    a_tr2 = inf ? a_tr2 : pf_a;
+                    v_tr2 = inf ? v_tr2 : pf_v;
+                    // next release: max(a_min, this task's S1 forward end)
+                    const double r_n = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
+                    r = inf ? r : r_n;
                 }
             }
         }
