@@ -35,6 +35,8 @@
 #endif
 #ifndef LMX_TILE_MINB
 #define LMX_TILE_MINB 4                     // resident CTAs/SM the register budget targets
+                                            // (2 for deep pipelines / several nodes per lane:
+                                            // their per-lane state would spill at 128 registers)
 #endif
 
 namespace lmx {
@@ -54,7 +56,7 @@ inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN :
 __host__ __device__ inline int cold_words(int S, bool scold) { return 2 * S + 3 + (scold ? 4 : 0); }
 
 template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, bool MEM>
-__global__ void __launch_bounds__(kBlock, LMX_TILE_MINB) event_loop_kernel(const KParams p)
+__global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_MINB) event_loop_kernel(const KParams p)
 {
     // LEMIX: the policy is LeMix (all candidates planned and scored); else one
     // of the baselines (RR / Separate / Fixed) picks the node first.
