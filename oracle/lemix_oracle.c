@@ -400,6 +400,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 
     /* ---- input validation (inputs must be finite, ordered and in range) ---- */
     int bad = (N < 1 || S < 1 || S > MAXS || nI < 0 || nT < 0 || par->qcap < 1 || !(par->lambda1 > 0.0));
+    bad = bad || par->sync_interval < 0 || !(par->sync_latency >= 0.0 && par->sync_latency < INFINITY);
     if (par->mem_enable)   /* Delta_t > 0 and T_max finite bound the wait loop */
         bad = bad || par->mem_cap < 0 || !(par->mem_dt > 0.0) || !(par->mem_tmax > 0.0 && par->mem_tmax < INFINITY) ||
               !(par->mem_pen >= 0.0 && par->mem_pen < INFINITY) || par->mem_tmax / par->mem_dt > 1048576.0;
@@ -429,6 +430,12 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
         T.node[n].q_train = (int64_t *)malloc((size_t)par->qcap * sizeof(int64_t));
     }
     uint32_t *defer = (uint32_t *)calloc((size_t)(n_tasks > 0 ? n_tasks : 1), sizeof(uint32_t));
+    /* Separate's checkpoints ([R-sync]): availability time on the inference
+     * nodes of checkpoint k = 1, 2, ... (taken when the (k*interval)-th
+     * training task in release order ends its backward) */
+    const int sync_sep = (par->policy == ORC_SEPARATE && par->sync_interval > 0);
+    double *ck_avail = (double *)malloc((size_t)(nT / (sync_sep ? par->sync_interval : 1) + 1) * sizeof(double));
+    int64_t n_ck = 0;
 
     /* Separate's partition ([R-20]) */
     int n_tr_nodes = 0, n_inf_nodes = N;
@@ -562,7 +569,16 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
                 counters->version_scan++;
                 if (T.path[nd->q_train[k]].eb[0] > p->sf[0]) pending++;
             }
-            sm.sum_version += nd->n_train_on - pending;
+            if (sync_sep) {
+                /* Separate: the newest checkpoint loaded on the inference node by
+                 * this task's forward start ([R-sync]) */
+                int64_t kmax = 0;
+                for (int64_t k = 0; k < n_ck; ++k)
+                    if (ck_avail[k] <= p->sf[0] && k + 1 > kmax) kmax = k + 1;
+                sm.sum_version += kmax * par->sync_interval;
+            } else {
+                sm.sum_version += nd->n_train_on - pending;
+            }
         }
         nd->last_task = task;
         nd->a_last = a;
@@ -588,6 +604,8 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
         counters->decisions++;
         if (is_train) {
             j++;
+            if (sync_sep && j % par->sync_interval == 0)               /* checkpoint ([R-sync]) */
+                ck_avail[n_ck++] = p->eb[0] + par->sync_latency;
             r = (j < nT) ? MAX(arrival[nI + j], p->ef[0]) : INFINITY;   /* PAPER.md:224 */
         } else {
             i++;
@@ -627,7 +645,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
     if (IIa != IIv) { free(IIa); free(Ra); free(fa); }
     free(sfv); free(efv);
     for (int n = 0; n < N; ++n) free(T.node[n].q_train);
-    free(T.node); free(T.path); free(defer);
+    free(T.node); free(T.path); free(defer); free(ck_avail);
     return status;
 }
 

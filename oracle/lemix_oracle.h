@@ -46,6 +46,12 @@ typedef struct {
     double mem_dt;                  /* check interval Delta_t */
     double mem_tmax;                /* maximum wait T_max */
     double mem_pen;                 /* offload penalty, seconds per offloaded token */
+    /* Separate's model synchronisation (
+     * DESIGN.md reading R-sync).  sync_interval = 0: every policy uses the
+     * co-located version proxy (R-ver). */
+    int32_t sync_interval;          /* checkpoint every this many training tasks (e.g. 100) */
+    int32_t sync_pad;
+    double sync_latency;            /* seconds from checkpoint to loaded on the inference nodes */
 } orc_params;
 
 /* Per-trace summary.  Integer block then fp64 block. */
