@@ -127,6 +127,18 @@ typedef struct {
     double mem_dt;         /* check interval Δ_t, seconds */
     double mem_tmax;       /* maximum wait T_max, seconds */
     double mem_pen;        /* offload penalty, seconds per offloaded token */
+    /* Separate's model synchronisation (DESIGN.md R-sync;
+     * SURVEY.md §8f NEXT-3): with policy LMX_SEPARATE and sync_interval > 0,
+     * a checkpoint is taken when every sync_interval-th training task (release
+     * order) ends its backward and is loaded on the inference nodes
+     * sync_latency seconds later; an inference task's version (summary
+     * sum_version) is the training count of the newest checkpoint loaded by
+     * its forward start.  0 (default): the co-located proxy (node's finished
+     * training tasks) for every policy.  sync_interval < 0 or sync_latency not
+     * finite and >= 0 -> LMX_EINVAL. */
+    int32_t sync_interval;
+    int32_t sync_pad;      /* zero */
+    double sync_latency;   /* seconds */
 } lmx_params;
 
 /* Per-trace summary (metrics of PAPER.md:786-790).  For a trace whose status

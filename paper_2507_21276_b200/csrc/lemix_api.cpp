@@ -155,6 +155,7 @@ struct lmx_ctx {
     // outputs / state
     int per_task = 1;
     DevBuf node_defer, decision_idx, completion, start_f1;
+    DevBuf ck;             // Separate's checkpoint lists (sync model)
     DevBuf summaries, trace_err, work, first_bad, ring_be;
     bool ran = false, synced = false;
 
@@ -197,6 +198,9 @@ void lmx_params_default(lmx_params *p)
     p->mem_dt = 0.0;
     p->mem_tmax = 0.0;
     p->mem_pen = 0.0;
+    p->sync_interval = 0;  // co-located version proxy for every policy
+    p->sync_pad = 0;
+    p->sync_latency = 0.0;
 }
 
 lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
@@ -380,6 +384,9 @@ lmx_status lmx_set_params(lmx_ctx *c, const lmx_params *p)
     if (!std::isfinite(p->lc0)) return c->fail(LMX_EINVAL, "params.lc0 must be finite");
     if (!(p->alpha >= 0.0 && p->alpha <= 1.0)) return c->fail(LMX_EINVAL, "params.alpha must be in [0, 1]");
     if (p->mem_enable != 0 && p->mem_enable != 1) return c->fail(LMX_EINVAL, "params.mem_enable must be 0 or 1");
+    if (p->sync_interval < 0) return c->fail(LMX_EINVAL, "params.sync_interval must be >= 0");
+    if (!(p->sync_latency >= 0.0 && std::isfinite(p->sync_latency)))
+        return c->fail(LMX_EINVAL, "params.sync_latency must be finite and >= 0");
     if (p->mem_enable) {   // Algorithm 2: Delta_t > 0 and a finite T_max bound the wait loop
         if (p->mem_cap < 0) return c->fail(LMX_EINVAL, "params.mem_cap must be >= 0");
         if (!(p->mem_dt > 0.0 && std::isfinite(p->mem_dt))) return c->fail(LMX_EINVAL, "params.mem_dt must be finite and > 0");
@@ -480,6 +487,9 @@ lmx_status lmx_run(lmx_ctx *c)
     k.mem_dt = P.mem_dt;
     k.mem_tmax = P.mem_tmax;
     k.mem_pen = P.mem_pen;
+    k.sync_sep = (P.policy == LMX_SEPARATE && P.sync_interval > 0) ? 1 : 0;
+    k.sync_interval = P.sync_interval > 0 ? P.sync_interval : 1;
+    k.sync_latency = P.sync_latency;
     k.n_traces = T;
     k.offsets = (const int64_t *)c->offsets.p;
     k.n_inf = (const int32_t *)c->n_inf.p;
@@ -526,6 +536,16 @@ lmx_status lmx_run(lmx_ctx *c)
     const size_t ring_entries = (size_t)tiles * k.npad * K;
     if (c->ring_be.ensure(ring_entries * lmx::ring_words(c->S, P.mem_enable != 0) * sizeof(double2)) != cudaSuccess)
         return c->fail(LMX_ENOMEM, "queue ring allocation (" + std::to_string(ring_entries) + " entries; lower qcap)");
+    if (k.sync_sep) {   // checkpoint list per tile slot: at most max_train / interval entries
+        int64_t max_train = 0;
+        for (int64_t t = 0; t < T; ++t)
+            max_train = std::max<int64_t>(max_train, c->h_offsets[t + 1] - c->h_offsets[t] - c->h_n_inf[t]);
+        const int64_t cap = max_train / k.sync_interval + 1;
+        if (cap > INT32_MAX || c->ck.ensure((size_t)tiles * cap * sizeof(double)) != cudaSuccess)
+            return c->fail(LMX_ENOMEM, "checkpoint list allocation");
+        k.ck = (double *)c->ck.p;
+        k.ck_cap = (int32_t)cap;
+    }
     if (c->summaries.ensure(std::max<int64_t>(T, 1) * sizeof(lmx_summary)) != cudaSuccess ||
         c->trace_err.ensure(std::max<int64_t>(T, 1) * 8) != cudaSuccess ||
         c->cell_i.ensure((size_t)c->n_cells * LMX_CELL_NI * 8) != cudaSuccess ||

@@ -28,6 +28,13 @@ struct KParams {
     int32_t mem_enable;
     long long mem_cap;
     double mem_dt, mem_tmax, mem_pen;
+    // Separate's checkpoint synchronisation (lmx_params.sync_*): sync_sep = 1
+    // when it applies; ck = per tile slot ck_cap doubles (availability times,
+    // kept as their suffix minima, non-decreasing)
+    int32_t sync_sep, sync_interval;
+    double sync_latency;
+    double *ck;
+    int32_t ck_cap;
 
     int64_t n_traces;
     const int64_t *offsets;    // device [n_traces+1]

@@ -126,6 +126,8 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
         dev::wait_inputs(p.ready, p.chunk_tasks, o, o + nI + nT);
 
         int i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0, cur_defer = 0;
+        int n_ck = 0;   // Separate's checkpoints so far (sync model, DESIGN.md R-sync)
+        double *ckt = p.sync_sep ? p.ck + gthread * p.ck_cap : nullptr;
         int status = LMX_OK, err_task = 0, err_code = kErrNone;
         double t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
         long long n_slo = 0, sum_ver = 0, n_def = 0;
@@ -384,6 +386,14 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                     while (k < qhb + qnb && qb.at(k, 0).y <= st0_b) k++;
                     VP_(best) = k;
                     ver = NTR_(best) - (qhb + qnb - k);
+                    if (p.sync_sep) {   // Separate: newest checkpoint loaded by start_f^1
+                        int lo_k = 0, hi_k = n_ck;
+                        while (lo_k < hi_k) {
+                            const int mid = (lo_k + hi_k) >> 1;
+                            if (ckt[mid] <= st0_b) lo_k = mid + 1; else hi_k = mid;
+                        }
+                        ver = lo_k * p.sync_interval;
+                    }
                 }
                 if (status == LMX_OK) {
                     {   // P, a_[-1], Eq. 2 history of the chosen node
@@ -430,6 +440,12 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                         if (j + 1 < nT) {
                             a_tr2 = __ldg(p.arrival + o + nI + j + 1);
                             v_tr2 = __ldg(p.lbk + o + nI + j + 1);
+                        }
+                        if (p.sync_sep && j % p.sync_interval == 0) {   // checkpoint (R-sync)
+                            const double av = done + p.sync_latency;
+                            ckt[n_ck] = av;
+                            for (int k = n_ck - 1; k >= 0 && ckt[k] > av; --k) ckt[k] = av;
+                            n_ck++;
                         }
                         r = (j < nT) ? dmax(a_tr, en_b[0]) : kInf;      // release
                     } else {

@@ -140,6 +140,8 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     double r = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
     long long n_slo = 0, sum_ver = 0, n_def = 0;
     int n_mwait = 0, n_moff = 0;          // Algorithm 2 counters (MEM)
+    int n_ck = 0;                         // Separate's checkpoints so far (sync model)
+    double *ckt = (!LEMIX && p.sync_sep) ? p.ck + gtile * p.ck_cap : nullptr;
     double a_inf = 0.0, a_inf2 = 0.0, a_tr = 0.0, a_tr2 = 0.0;   // 2-deep input prefetch
     uint32_t v_inf = 0, v_inf2 = 0, v_tr = 0, v_tr2 = 0;
 
@@ -176,6 +178,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 dev::sts_l(c_tw(3), kErrNone);
                 n_slo = sum_ver = n_def = 0;
                 n_mwait = n_moff = 0;
+                n_ck = 0;
                 sum_ttft = 0.0;
                 t_last = -kInf;
                 a_last_inf = -kInf;
@@ -569,6 +572,18 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                                 while (k < tail && q.at(k, 0).y <= c_st0) k++;
                                 vp = k;
                                 c_ver = ntr - (tail - k);
+                                if (!LEMIX && p.sync_sep) {
+                                    // Separate: training count of the newest checkpoint loaded
+                                    // by this forward start (DESIGN.md R-sync): the list holds
+                                    // suffix minima of the load times, non-decreasing, so the
+                                    // count of entries <= start_f^1 is that checkpoint's index
+                                    int lo_k = 0, hi_k = n_ck;
+                                    while (lo_k < hi_k) {
+                                        const int mid = (lo_k + hi_k) >> 1;
+                                        if (ckt[mid] <= c_st0) lo_k = mid + 1; else hi_k = mid;
+                                    }
+                                    c_ver = lo_k * p.sync_interval;
+                                }
                             }
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
@@ -648,6 +663,15 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                     v_tr = inf ? v_tr : v_tr2;
                     a_tr2 = inf ? a_tr2 : pf_a;
                     v_tr2 = inf ? v_tr2 : pf_v;
+                    if (!LEMIX && p.sync_sep && !inf && j % p.sync_interval == 0) {
+                        // Separate: checkpoint after this training task's backward, loaded
+                        // sync_latency later (R-sync); every lane of the tile
+                        // writes the same values (each reads back only its own writes)
+                        const double av = c_done + p.sync_latency;
+                        ckt[n_ck] = av;
+                        for (int k = n_ck - 1; k >= 0 && ckt[k] > av; --k) ckt[k] = av;   // suffix minima
+                        n_ck++;
+                    }
                     // next release: max(a_min, this task's S1 forward end)
                     const double r_n = (j < nT) ? dev::dmax(a_tr, c_en0) : kInf;
                     r = inf ? r : r_n;

@@ -17,7 +17,8 @@ def oracle_params(lp) -> oracle.OracleParams:
                                slo_mult=lp.slo_mult, sigma_floor=lp.sigma_floor, lc0=lp.lc0, alpha=lp.alpha,
                                deprioritize=lp.deprioritize, slo_mode=lp.slo_mode, qcap=lp.qcap,
                                slo_const=lp.slo_const, mem_enable=lp.mem_enable, mem_cap=lp.mem_cap,
-                               mem_dt=lp.mem_dt, mem_tmax=lp.mem_tmax, mem_pen=lp.mem_pen)
+                               mem_dt=lp.mem_dt, mem_tmax=lp.mem_tmax, mem_pen=lp.mem_pen,
+                               sync_interval=lp.sync_interval, sync_latency=lp.sync_latency)
 
 
 def rel_err(a, b):

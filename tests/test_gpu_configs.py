@@ -193,3 +193,21 @@ def test_sharded_runs_equal_single_run(world):
         assert np.array_equal(acc[k], whole.cells[k]), k
     for k in lemix.CELL_F64:
         np.testing.assert_allclose(acc[k], whole.cells[k], rtol=1e-12, err_msg=k)
+
+
+def test_sweep_separate_sync_full_size_sampled():
+    """The sweep config (4096 traces x 16 rates) under Separate with
+    checkpoint synchronisation every 100 training tasks."""
+    N, S = 4, 2
+    parts = [workload.generate(workload.sweep_spec(rate), 4096, seed_base=1 + 4096 * k)
+             for k, rate in enumerate(workload.SWEEP_RATES)]
+    tr = workload.concat(parts)
+    lp = lemix.Params(policy=lemix.LMX_SEPARATE, sync_interval=100, sync_latency=1.5)
+    ef, eb = workload.profile(N, S)
+    g = lemix.run(ef, eb, N, S, tr, lp, outputs=True)
+    assert g.status == 0
+    idx = np.array([c * 4096 + k for c in range(16) for k in (0, 4095)])
+    sub, osum, opt = _oracle_subset(N, S, tr, idx, lp)
+    compare_summaries(g.summaries[idx], osum)
+    compare_tasks(sub, _gpu_subset_tasks(g, tr, idx), opt, osum)
+    assert osum["sum_version"].sum() > 0

@@ -136,3 +136,15 @@ def test_large_cluster_trace():
     N, S = 64, 8
     tr = workload.generate(workload.large_spec(rate=1600.0, n_inf=20000), 2, seed_base=5)
     check(N, S, tr, P(qcap=1024))
+
+
+# ---------------------------------------------------------------- Separate sync (NEXT-3)
+@pytest.mark.parametrize("interval,latency", [(1, 0.0), (3, 0.25), (10, 2.0), (100, 1.5)])
+def test_separate_checkpoint_sync(interval, latency):
+    """Separate's checkpoint-synchronisation version model (PAPER.md:665;
+    DESIGN.md R-sync): sum_version bit-exact against the oracle."""
+    parts = [workload.generate(workload.sweep_spec(rate), 8, seed_base=300 + 8 * k)
+             for k, rate in enumerate((20.0, 80.0, 160.0))]
+    tr = workload.concat(parts)
+    g, osum, _ = check(4, 2, tr, P(policy=lemix.LMX_SEPARATE, sync_interval=interval, sync_latency=latency))
+    assert (osum["sum_version"] > 0).any() or interval == 100
