@@ -198,6 +198,15 @@ lmx_status lmx_set_params(lmx_ctx *ctx, const lmx_params *params);
  * cell_of_trace[n_traces] in [0, n_cells)).  NULL / 1 = one cell. */
 lmx_status lmx_set_cells(lmx_ctx *ctx, const int32_t *cell_of_trace, int32_t n_cells);
 
+/* Optional (after lmx_set_cells with the same n_cells): per-cell values of
+ * Eq. 3's λ1, λ2 and Eq. 1's τ (host arrays [n_cells]; a NULL array keeps the
+ * lmx_params value), so one run sweeps the parameter study of PAPER.md
+ * Fig. 15.  n_cells = 0 clears them.  Values are
+ * validated like lmx_set_params (λ1 > 0, λ2 >= 0, finite) -> LMX_EINVAL;
+ * without matching cells -> LMX_ESTATE.  LeMix on the tile kernel only. */
+lmx_status lmx_set_cell_params(lmx_ctx *ctx, int32_t n_cells, const double *lambda1, const double *lambda2,
+                               const double *tau);
+
 /* Optional: keep per-task outputs (default on).  Off = summary-only runs. */
 lmx_status lmx_set_outputs(lmx_ctx *ctx, int per_task);
 

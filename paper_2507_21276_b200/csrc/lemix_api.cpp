@@ -156,6 +156,8 @@ struct lmx_ctx {
     int per_task = 1;
     DevBuf node_defer, decision_idx, completion, start_f1;
     DevBuf ck;             // Separate's checkpoint lists (sync model)
+    DevBuf cell_par;       // per-cell (lambda1, lambda2, tau)
+    int32_t n_cell_par = 0;
     DevBuf summaries, trace_err, work, first_bad, ring_be;
     bool ran = false, synced = false;
 
@@ -426,6 +428,36 @@ lmx_status lmx_set_cells(lmx_ctx *c, const int32_t *cell_of, int32_t n_cells)
     return LMX_OK;
 }
 
+lmx_status lmx_set_cell_params(lmx_ctx *c, int32_t n_cells, const double *l1, const double *l2, const double *tau)
+{
+    if (!c) return LMX_EINVAL;
+    if (n_cells == 0) {
+        c->n_cell_par = 0;
+        c->cell_par.release();
+        return LMX_OK;
+    }
+    if (!c->have_params) return c->fail(LMX_ESTATE, "lmx_set_cell_params: set params first");
+    if (!c->cells_set || c->n_cells != n_cells)
+        return c->fail(LMX_ESTATE, "lmx_set_cell_params: lmx_set_cells with the same n_cells first");
+    std::vector<double> h((size_t)n_cells * 3);
+    for (int32_t k = 0; k < n_cells; ++k) {
+        const double a = l1 ? l1[k] : c->par.lambda1, b = l2 ? l2[k] : c->par.lambda2, t = tau ? tau[k] : c->par.tau;
+        if (!(a > 0.0 && std::isfinite(a)) || !(b >= 0.0 && std::isfinite(b)) || !std::isfinite(t))
+            return c->fail(LMX_EINVAL, "cell params[" + std::to_string(k) + "]: lambda1 > 0, lambda2 >= 0, tau finite");
+        h[3 * k] = a;
+        h[3 * k + 1] = b;
+        h[3 * k + 2] = t;
+    }
+    cudaSetDevice(c->device);
+    if (c->cell_par.ensure(h.size() * sizeof(double)) != cudaSuccess) return c->fail(LMX_ENOMEM, "cell params");
+    lmx_status s = c->cuda(cudaMemcpyAsync(c->cell_par.p, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                           c->stream), "cell params copy");
+    if (s == LMX_OK) s = c->cuda(cudaStreamSynchronize(c->stream), "cell params copy");
+    if (s != LMX_OK) return s;
+    c->n_cell_par = n_cells;
+    return LMX_OK;
+}
+
 lmx_status lmx_set_outputs(lmx_ctx *c, int per_task)
 {
     if (!c) return LMX_EINVAL;
@@ -490,6 +522,12 @@ lmx_status lmx_run(lmx_ctx *c)
     k.sync_sep = (P.policy == LMX_SEPARATE && P.sync_interval > 0) ? 1 : 0;
     k.sync_interval = P.sync_interval > 0 ? P.sync_interval : 1;
     k.sync_latency = P.sync_latency;
+    if (c->n_cell_par > 0) {
+        if (!c->cells_set || c->n_cells != c->n_cell_par)
+            return c->fail(LMX_ESTATE, "lmx_run: cell params need lmx_set_cells with the same n_cells");
+        k.cell_par = (const double *)c->cell_par.p;
+        k.cell_of = (const int32_t *)c->cell_of.p;
+    }
     k.n_traces = T;
     k.offsets = (const int64_t *)c->offsets.p;
     k.n_inf = (const int32_t *)c->n_inf.p;
@@ -507,6 +545,8 @@ lmx_status lmx_run(lmx_ctx *c)
                 return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: not supported for this N x S");
             if (P.mem_enable)
                 return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: the memory model (Algorithm 2) runs on the tile kernel only");
+            if (c->n_cell_par > 0)
+                return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: per-cell parameters run on the tile kernel only");
             lane = true;
         }
     }

@@ -35,6 +35,9 @@ struct KParams {
     double sync_latency;
     double *ck;
     int32_t ck_cap;
+    // per-cell (lambda1, lambda2, tau) of lmx_set_cell_params, or nullptr
+    const double *cell_par;
+    const int32_t *cell_of;
 
     int64_t n_traces;
     const int64_t *offsets;    // device [n_traces+1]

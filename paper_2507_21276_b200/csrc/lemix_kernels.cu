@@ -110,7 +110,7 @@ int event_loop_smem_bytes(const KParams &p)
     const int W = tile::window_entries(p.S);
     const int npl = npl_bucket(p.npl);
     return 16 * p.N * p.S + (W > 0 ? kBlock * npl * W * ring_words(p.S, p.mem_enable != 0) * 16 : 0) +
-           kBlock * (npl * tile::cold_words(p.S, npl > 1) + 4) * 8;
+           kBlock * (npl * tile::cold_words(p.S, npl > 1) + (p.cell_par ? tile::kTraceWords : 4)) * 8;
 }
 
 int event_loop_block_threads() { return kBlock; }

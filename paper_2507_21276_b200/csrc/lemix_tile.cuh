@@ -43,6 +43,7 @@ namespace lmx {
 namespace tile {
 
 constexpr int kBlock = 128;                 // 4 warps per CTA
+constexpr int kTraceWords = 7;              // rarely used per-trace shared-memory words (c_tw; 4 without cell params)
 using dev::kInf;
 using dev::task_batch;
 using dev::task_len;
@@ -68,6 +69,9 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     // S is a compile-time constant when it equals the template bucket (EXACT)
     const int N = p.N, S = EXACT ? SMAX : p.S, NS = p.N * S;
     double *s_eta = reinterpret_cast<double *>(smem_raw);
+    // per-cell parameters (lmx_set_cell_params) are read by the generic-width
+    // LeMix instantiations; the host picks one of those when they are set
+    constexpr bool CPAR = LEMIX && TT == 0;
 
     // ---- K1: stage eta_f | eta_b (16*N*S bytes) into shared memory via TMA ----
     if (threadIdx.x == 0) {
@@ -124,7 +128,8 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     auto c_sl2 = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 1) * cstride; };
     auto c_ntr = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 2) * cstride; };
     // rarely used per-trace words (same column layout, after the node slots):
-    // 0 trace index, 1 first task offset, 2 t_first, 3 error (task << 8 | field)
+    // 0 trace index, 1 first task offset, 2 t_first, 3 error (task << 8 | field),
+    // 4-6 the trace's cell (lambda1, lambda2, tau) with lmx_set_cell_params
     auto c_tw = [&](int k) { return cbase + (uint32_t)(NPL * CW + k) * cstride; };
     // SCOLD (several nodes per lane): a_[-1], mu, 1/(2 sigma^2), 1/(sigma sqrt(2 pi))
     // of each node also live in shared memory (read once per decision)
@@ -191,6 +196,12 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 if (nI > 0) t_first = dev::dmin(t_first, a_inf);
                 if (nT > 0) t_first = dev::dmin(t_first, a_tr);
                 dev::sts_d(c_tw(2), t_first);
+                if (CPAR && p.cell_par) {    // the trace's cell parameters (NEXT-4 sweeps)
+                    const double *cp = p.cell_par + 3 * p.cell_of[t];
+                    dev::sts_d(c_tw(4), cp[0]);
+                    dev::sts_d(c_tw(5), cp[1]);
+                    dev::sts_d(c_tw(6), cp[2]);
+                }
 #pragma unroll
                 for (int jj = 0; jj < NPL; ++jj) {
                     hasp[jj] = qh[jj] = qn[jj] = cnt[jj] = 0;
@@ -456,8 +467,12 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                             const double ap_j = SCOLD ? dev::lds_d(c_sc(jj, 0)) : aprev[jj];
                             const double a_last = hasp[jj] ? ap_j : a;                   // R-9
                             const double IIS = p.s_pow2 ? II * p.inv_S : II / (double)S;  // exact either way
-                            const double IP = -dev::dmax(IIS - (a - a_last), p.tau);      // Eq. 1
-                            const double f = (IP + p.lambda2 * LC) / (p.lambda1 * R);     // Eq. 3
+                            const bool cpar = CPAR && p.cell_par != nullptr;              // (uniform)
+                            const double lam1 = cpar ? dev::lds_d(c_tw(4)) : p.lambda1;
+                            const double lam2 = cpar ? dev::lds_d(c_tw(5)) : p.lambda2;
+                            const double tau = cpar ? dev::lds_d(c_tw(6)) : p.tau;
+                            const double IP = -dev::dmax(IIS - (a - a_last), tau);        // Eq. 1
+                            const double f = (IP + lam2 * LC) / (lam1 * R);               // Eq. 3
                             if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
                         }
                         {   // speculative statistics: count cnt+1, sums + l, + l^2
@@ -702,7 +717,7 @@ kernel_fn pick(const KParams &p)
     case 1: return pick_npl<1, true, LEMIX, MEM>(nb);
     case 2:
         // the bench shape (4 nodes x 2 stages): tile width fixed at compile time
-        if (p.S == 2 && nb == 1 && p.T == 4) return event_loop_kernel<2, true, 1, LEMIX, 4, MEM>;
+        if (p.S == 2 && nb == 1 && p.T == 4 && !p.cell_par) return event_loop_kernel<2, true, 1, LEMIX, 4, MEM>;
         return p.S == 2 ? pick_npl<2, true, LEMIX, MEM>(nb) : pick_npl<2, false, LEMIX, MEM>(nb);
     case 4: return p.S == 4 ? pick_npl<4, true, LEMIX, MEM>(nb) : pick_npl<4, false, LEMIX, MEM>(nb);
     case 8: return p.S == 8 ? pick_npl<8, true, LEMIX, MEM>(nb) : pick_npl<8, false, LEMIX, MEM>(nb);

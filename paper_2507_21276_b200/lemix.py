@@ -24,7 +24,7 @@ STATUS_NAMES = {0: "LMX_OK", 1: "LMX_EINVAL", 2: "LMX_ESTATE", 3: "LMX_ENOMEM", 
                 5: "LMX_ENCCL", 6: "LMX_EQCAP", 7: "LMX_EBUDGET"}
 
 EXPORTS = ("lmx_params_default", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_load_profile",
-           "lmx_load_traces", "lmx_set_params", "lmx_set_cells", "lmx_set_outputs", "lmx_run", "lmx_sync",
+           "lmx_load_traces", "lmx_set_params", "lmx_set_cells", "lmx_set_cell_params", "lmx_set_outputs", "lmx_run", "lmx_sync",
            "lmx_get_assignments", "lmx_get_times", "lmx_get_summaries", "lmx_get_cells",
            "lmx_allreduce_cells", "lmx_nccl_unique_id", "lmx_nccl_comm_init", "lmx_nccl_comm_destroy",
            "lmx_get_timing", "lmx_get_geometry")
@@ -83,6 +83,7 @@ def load_library():
         "lmx_load_traces": (st, [vp, ctypes.POINTER(lmx_traces), ctypes.c_int]),
         "lmx_set_params": (st, [vp, ctypes.POINTER(lmx_params)]),
         "lmx_set_cells": (st, [vp, vp, i32]),
+        "lmx_set_cell_params": (st, [vp, i32, vp, vp, vp]),
         "lmx_set_outputs": (st, [vp, ctypes.c_int]),
         "lmx_run": (st, [vp]),
         "lmx_sync": (st, [vp]),
@@ -203,6 +204,10 @@ class Context:
         arr = None if cell_of_trace is None else np.ascontiguousarray(cell_of_trace, np.int32)
         return self._check(self.lib.lmx_set_cells(self.h, _ptr(arr), n_cells))
 
+    def lmx_set_cell_params(self, n_cells, lambda1=None, lambda2=None, tau=None):
+        arrs = [None if a is None else np.ascontiguousarray(a, np.float64) for a in (lambda1, lambda2, tau)]
+        return self._check(self.lib.lmx_set_cell_params(self.h, n_cells, *[_ptr(a) for a in arrs]))
+
     def lmx_set_outputs(self, per_task: bool):
         return self._check(self.lib.lmx_set_outputs(self.h, 1 if per_task else 0))
 
@@ -292,7 +297,8 @@ class RunResult:
 
 
 def run(eta_f, eta_b, n_nodes, n_stages, traces, params: Params | None = None, device: int = 0,
-        outputs: bool = True, fixed_node=None, cells=None, n_cells: int = 1, ctx: Context | None = None):
+        outputs: bool = True, fixed_node=None, cells=None, n_cells: int = 1, ctx: Context | None = None,
+        cell_params: dict | None = None):
     """Convenience: create -> load -> run -> sync -> fetch, all through the C ABI.
     `traces` is a workload.Traces (host arrays)."""
     params = params or Params()
@@ -305,6 +311,8 @@ def run(eta_f, eta_b, n_nodes, n_stages, traces, params: Params | None = None, d
                             None if fixed_node is None else np.ascontiguousarray(fixed_node, np.int32))
         ctx.lmx_set_params(params)
         ctx.lmx_set_cells(cells, n_cells)
+        if cell_params is not None:   # {"lambda1": [...], "lambda2": [...], "tau": [...]} per cell
+            ctx.lmx_set_cell_params(n_cells, **cell_params)
         ctx.lmx_set_outputs(outputs)
         ctx.lmx_run()
         st = ctx.lmx_sync()

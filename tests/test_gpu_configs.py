@@ -211,3 +211,25 @@ def test_sweep_separate_sync_full_size_sampled():
     compare_summaries(g.summaries[idx], osum)
     compare_tasks(sub, _gpu_subset_tasks(g, tr, idx), opt, osum)
     assert osum["sum_version"].sum() > 0
+
+
+def test_parameter_sweep_cells():
+    """NEXT-4 parameter study (Fig. 15, lambda1 / lambda2 / tau):
+    one run with per-cell parameters equals, trace by trace, the oracle run
+    with each cell's parameters."""
+    N, S = 4, 2
+    grid = [(l1, l2, tau) for l1 in (0.5, 1.0, 4.0) for l2 in (0.0, 1.0, 10.0) for tau in (-0.02, 0.0, 0.05)]
+    K = len(grid)
+    tr = workload.generate(workload.sweep_spec(120.0), 4 * K, seed_base=900)
+    cells = np.repeat(np.arange(K, dtype=np.int32), 4)
+    ef, eb = workload.profile(N, S)
+    cp = {"lambda1": [g[0] for g in grid], "lambda2": [g[1] for g in grid], "tau": [g[2] for g in grid]}
+    g = lemix.run(ef, eb, N, S, tr, lemix.Params(), outputs=True, cells=cells, n_cells=K, cell_params=cp)
+    assert g.status == 0
+    for k, (l1, l2, tau) in enumerate(grid):
+        idx = np.nonzero(cells == k)[0]
+        sub, osum, opt = _oracle_subset(N, S, tr, idx, lemix.Params(lambda1=l1, lambda2=l2, tau=tau))
+        compare_summaries(g.summaries[idx], osum)
+        compare_tasks(sub, _gpu_subset_tasks(g, tr, idx), opt, osum)
+    # the cells differ (the parameters matter)
+    assert len({g.summaries["n_slo_met"][cells == k].sum() for k in range(K)}) > 1
