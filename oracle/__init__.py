@@ -36,7 +36,9 @@ class Params(ctypes.Structure):
                 ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double),
                 ("mem_enable", ctypes.c_int32), ("mem_pad", ctypes.c_int32), ("mem_cap", ctypes.c_int64),
                 ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double),
-                ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double)]
+                ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double),
+                ("sep_dynamic", ctypes.c_int32), ("sep_pad", ctypes.c_int32), ("dyn_rate", ctypes.c_double),
+                ("dyn_window", ctypes.c_double)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes",
@@ -103,12 +105,17 @@ class OracleParams:
     # Separate's checkpoint synchronisation (NEXT-3, DESIGN.md R-sync); 0 = off
     sync_interval: int = 0
     sync_latency: float = 0.0
+    # SeparateDynamic (NEXT-3, DESIGN.md R-sepdyn); 0 = static alpha partition
+    sep_dynamic: int = 0
+    dyn_rate: float = 50.0
+    dyn_window: float = 10.0
 
     def _c(self) -> Params:
         return Params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1,
                       self.lambda2, self.tau, self.slo_mult, self.slo_const, self.sigma_floor,
                       self.lc0, self.alpha, self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax,
-                      self.mem_pen, self.sync_interval, 0, self.sync_latency)
+                      self.mem_pen, self.sync_interval, 0, self.sync_latency, self.sep_dynamic, 0, self.dyn_rate,
+                      self.dyn_window)
 
 
 def _ptr(a):

@@ -401,6 +401,9 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
     /* ---- input validation (inputs must be finite, ordered and in range) ---- */
     int bad = (N < 1 || S < 1 || S > MAXS || nI < 0 || nT < 0 || par->qcap < 1 || !(par->lambda1 > 0.0));
     bad = bad || par->sync_interval < 0 || !(par->sync_latency >= 0.0 && par->sync_latency < INFINITY);
+    if (par->sep_dynamic)
+        bad = bad || !(par->dyn_rate >= 0.0 && par->dyn_rate < INFINITY) ||
+              !(par->dyn_window > 0.0 && par->dyn_window < INFINITY);
     if (par->mem_enable)   /* Delta_t > 0 and T_max finite bound the wait loop */
         bad = bad || par->mem_cap < 0 || !(par->mem_dt > 0.0) || !(par->mem_tmax > 0.0 && par->mem_tmax < INFINITY) ||
               !(par->mem_pen >= 0.0 && par->mem_pen < INFINITY) || par->mem_tmax / par->mem_dt > 1048576.0;
@@ -449,6 +452,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
     /* ---- the global queue: inference by arrival, training released at the
      * previous training task's S1 forward end ([R-18]) ---- */
     int64_t i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0;
+    int64_t rate_lo = 0, rate_hi = 0;   /* SeparateDynamic: arrivals in (now - W, now] */
     double r = (nT > 0) ? arrival[nI] : INFINITY;
     double t_last = -INFINITY;
     int status = ORC_OK;
@@ -515,10 +519,18 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
             } else if (par->policy == ORC_SEPARATE) {
                 if (n_tr_nodes == 0) {                                    /* one kind only */
                     if (is_train) best = (int)(sep_t++ % N); else best = (int)(sep_i++ % N);
-                } else if (is_train) {
-                    best = n_inf_nodes + (int)(sep_t++ % n_tr_nodes);
                 } else {
-                    best = (int)(sep_i++ % n_inf_nodes);
+                    int ninf = n_inf_nodes;
+                    if (par->sep_dynamic) {
+                        /* request rate over the last dyn_window seconds ([R-sepdyn]) */
+                        while (rate_hi < nI && arrival[rate_hi] <= now) rate_hi++;
+                        const double w_lo = now - par->dyn_window;
+                        while (rate_lo < nI && arrival[rate_lo] <= w_lo) rate_lo++;
+                        const double rate = (double)(rate_hi - rate_lo) / par->dyn_window;
+                        ninf = (rate < par->dyn_rate) ? (N / 4 > 1 ? N / 4 : 1) : n_inf_nodes;  /* "1-3" : "2-2" */
+                    }
+                    if (is_train) best = ninf + (int)(sep_t++ % (N - ninf));
+                    else best = (int)(sep_i++ % ninf);
                 }
             } else {
                 best = fixed_node[task];

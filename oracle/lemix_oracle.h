@@ -52,6 +52,14 @@ typedef struct {
     int32_t sync_interval;          /* checkpoint every this many training tasks (e.g. 100) */
     int32_t sync_pad;
     double sync_latency;            /* seconds from checkpoint to loaded on the inference nodes */
+    /* SeparateDynamic (reading R-sepdyn): the
+     * partition follows the request rate over (now - dyn_window, now]:
+     * below dyn_rate one inference node ("1-3" at N = 4, max(1, N/4) in
+     * general), otherwise the alpha partition ("2-2"). */
+    int32_t sep_dynamic;
+    int32_t sep_pad;
+    double dyn_rate;                /* requests/s threshold (50 in the paper) */
+    double dyn_window;              /* seconds */
 } orc_params;
 
 /* Per-trace summary.  Integer block then fp64 block. */

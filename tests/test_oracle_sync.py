@@ -47,3 +47,23 @@ def test_sync_off_keeps_the_colocated_proxy():
     c = oracle.run_batch(ef, eb, 4, 2, tr, oracle.OracleParams())[0]
     d = oracle.run_batch(ef, eb, 4, 2, tr, oracle.OracleParams(sync_interval=2, sync_latency=1.0))[0]
     assert c.tobytes() == d.tobytes()
+
+
+def test_separate_dynamic_limits():
+    """SeparateDynamic (R-sepdyn) with a threshold of 0 never
+    switches to 1-3 (the static alpha partition); with a huge threshold it
+    always runs 1-3: inference on node 0 only, training on the other nodes."""
+    tr = workload.generate(workload.sweep_spec(100.0, tasks=300), 3, seed_base=17)
+    ef, eb = workload.profile(4, 2)
+    static = oracle.run_batch(ef, eb, 4, 2, tr, oracle.OracleParams(policy=oracle.SEPARATE))
+    never = oracle.run_batch(ef, eb, 4, 2, tr, oracle.OracleParams(policy=oracle.SEPARATE, sep_dynamic=1,
+                                                                     dyn_rate=0.0, dyn_window=5.0))
+    assert np.array_equal(static[1]["node_defer"], never[1]["node_defer"])
+    always = oracle.run_batch(ef, eb, 4, 2, tr, oracle.OracleParams(policy=oracle.SEPARATE, sep_dynamic=1,
+                                                                      dyn_rate=1e30, dyn_window=5.0))
+    node = always[1]["node_defer"] & 0xFFFF
+    for t in range(tr.n_traces):
+        a, b = tr.offsets[t], tr.offsets[t + 1]
+        nI = tr.n_inf[t]
+        assert set(node[a:a + nI]) == {0}
+        assert set(node[a + nI:b]) == {1, 2, 3}
