@@ -139,6 +139,16 @@ typedef struct {
     int32_t sync_interval;
     int32_t sync_pad;      /* zero */
     double sync_latency;   /* seconds */
+    /* SeparateDynamic (DESIGN.md R-sepdyn; NEXT-3): with policy
+     * LMX_SEPARATE and sep_dynamic = 1 the partition follows the inference
+     * request rate over (now - dyn_window, now]: below dyn_rate requests/s
+     * max(1, N/4) inference nodes ("1-3" at N = 4), otherwise the alpha
+     * partition ("2-2").  dyn_rate not finite and >= 0 or dyn_window not
+     * finite and > 0 (when enabled) -> LMX_EINVAL. */
+    int32_t sep_dynamic;
+    int32_t sep_pad;       /* zero */
+    double dyn_rate;       /* requests/s (50 in the paper) */
+    double dyn_window;     /* seconds */
 } lmx_params;
 
 /* Per-trace summary (metrics of PAPER.md:786-790).  For a trace whose status

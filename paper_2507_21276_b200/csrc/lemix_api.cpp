@@ -203,6 +203,10 @@ void lmx_params_default(lmx_params *p)
     p->sync_interval = 0;  // co-located version proxy for every policy
     p->sync_pad = 0;
     p->sync_latency = 0.0;
+    p->sep_dynamic = 0;    // static alpha partition
+    p->sep_pad = 0;
+    p->dyn_rate = 50.0;
+    p->dyn_window = 10.0;
 }
 
 lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
@@ -389,6 +393,11 @@ lmx_status lmx_set_params(lmx_ctx *c, const lmx_params *p)
     if (p->sync_interval < 0) return c->fail(LMX_EINVAL, "params.sync_interval must be >= 0");
     if (!(p->sync_latency >= 0.0 && std::isfinite(p->sync_latency)))
         return c->fail(LMX_EINVAL, "params.sync_latency must be finite and >= 0");
+    if (p->sep_dynamic != 0 && p->sep_dynamic != 1) return c->fail(LMX_EINVAL, "params.sep_dynamic must be 0 or 1");
+    if (p->sep_dynamic && !(p->dyn_rate >= 0.0 && std::isfinite(p->dyn_rate)))
+        return c->fail(LMX_EINVAL, "params.dyn_rate must be finite and >= 0");
+    if (p->sep_dynamic && !(p->dyn_window > 0.0 && std::isfinite(p->dyn_window)))
+        return c->fail(LMX_EINVAL, "params.dyn_window must be finite and > 0");
     if (p->mem_enable) {   // Algorithm 2: Delta_t > 0 and a finite T_max bound the wait loop
         if (p->mem_cap < 0) return c->fail(LMX_EINVAL, "params.mem_cap must be >= 0");
         if (!(p->mem_dt > 0.0 && std::isfinite(p->mem_dt))) return c->fail(LMX_EINVAL, "params.mem_dt must be finite and > 0");
@@ -522,6 +531,9 @@ lmx_status lmx_run(lmx_ctx *c)
     k.sync_sep = (P.policy == LMX_SEPARATE && P.sync_interval > 0) ? 1 : 0;
     k.sync_interval = P.sync_interval > 0 ? P.sync_interval : 1;
     k.sync_latency = P.sync_latency;
+    k.sep_dynamic = (P.policy == LMX_SEPARATE && P.sep_dynamic) ? 1 : 0;
+    k.dyn_rate = P.dyn_rate;
+    k.dyn_window = P.dyn_window;
     if (c->n_cell_par > 0) {
         if (!c->cells_set || c->n_cells != c->n_cell_par)
             return c->fail(LMX_ESTATE, "lmx_run: cell params need lmx_set_cells with the same n_cells");

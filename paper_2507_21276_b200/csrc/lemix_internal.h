@@ -33,6 +33,9 @@ struct KParams {
     // kept as their suffix minima, non-decreasing)
     int32_t sync_sep, sync_interval;
     double sync_latency;
+    // SeparateDynamic (lmx_params.sep_dynamic): rate threshold and window
+    int32_t sep_dynamic;
+    double dyn_rate, dyn_window;
     double *ck;
     int32_t ck_cap;
     // per-cell (lambda1, lambda2, tau) of lmx_set_cell_params, or nullptr

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
 
         int i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0, cur_defer = 0;
         int n_ck = 0;   // Separate's checkpoints so far (sync model, DESIGN.md R-sync)
+        int rate_lo = 0, rate_hi = 0;   // SeparateDynamic window pointers
         double *ckt = p.sync_sep ? p.ck + gthread * p.ck_cap : nullptr;
         int status = LMX_OK, err_task = 0, err_code = kErrNone;
         double t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
@@ -293,8 +294,17 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
                         rr++;
                     } else if (p.policy == LMX_SEPARATE) {
                         if (!(nI > 0 && nT > 0)) best = is_train ? (sep_t++ % N) : (sep_i++ % N);
-                        else if (is_train) best = (N - p.n_tr_sep) + (sep_t++ % p.n_tr_sep);
-                        else best = sep_i++ % (N - p.n_tr_sep);
+                        else {
+                            int ninf = N - p.n_tr_sep;
+                            if (p.sep_dynamic) {   // SeparateDynamic (R-sepdyn)
+                                while (rate_hi < nI && __ldg(p.arrival + o + rate_hi) <= now) rate_hi++;
+                                const double w_lo = now - p.dyn_window;
+                                while (rate_lo < nI && __ldg(p.arrival + o + rate_lo) <= w_lo) rate_lo++;
+                                const double rate = (double)(rate_hi - rate_lo) / p.dyn_window;
+                                ninf = (rate < p.dyn_rate) ? (N / 4 > 1 ? N / 4 : 1) : ninf;
+                            }
+                            best = is_train ? ninf + (sep_t++ % (N - ninf)) : (sep_i++ % ninf);
+                        }
                     } else {
                         best = __ldg(p.fixed + o + task);
                     }

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     const double *tarr = p.arrival;      // this trace's task arrays (32-bit indexing)
     const uint32_t *tlbk = p.lbk;
     int nI = 0, nT = 0, i = 0, j = 0, step = 0, iters = 0, rr = 0, sep_i = 0, sep_t = 0;
+    int rate_lo = 0, rate_hi = 0;         // SeparateDynamic: inference arrivals in (now - W, now]
     int cur_defer = 0, status = LMX_OK;
     double r = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
     long long n_slo = 0, sum_ver = 0, n_def = 0;
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 tarr = p.arrival + o;
                 tlbk = p.lbk + o;
                 i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
+                rate_lo = rate_hi = 0;
                 status = LMX_OK;
                 dev::sts_l(c_tw(0), t);
                 dev::sts_l(c_tw(1), o);
@@ -409,10 +411,18 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 } else if (p.policy == LMX_SEPARATE) {
                     if (!(nI > 0 && nT > 0)) {
                         chosen = is_train ? (sep_t++ % N) : (sep_i++ % N);
-                    } else if (is_train) {
-                        chosen = (N - p.n_tr_sep) + (sep_t++ % p.n_tr_sep);
                     } else {
-                        chosen = sep_i++ % (N - p.n_tr_sep);
+                        int ninf = N - p.n_tr_sep;
+                        if (p.sep_dynamic) {
+                            // SeparateDynamic (R-sepdyn): request rate over
+                            // the last dyn_window seconds -> "1-3" or the alpha partition
+                            while (rate_hi < nI && __ldg(tarr + rate_hi) <= now) rate_hi++;
+                            const double w_lo = now - p.dyn_window;
+                            while (rate_lo < nI && __ldg(tarr + rate_lo) <= w_lo) rate_lo++;
+                            const double rate = (double)(rate_hi - rate_lo) / p.dyn_window;
+                            ninf = (rate < p.dyn_rate) ? (N / 4 > 1 ? N / 4 : 1) : ninf;
+                        }
+                        chosen = is_train ? ninf + (sep_t++ % (N - ninf)) : (sep_i++ % ninf);
                     }
                 } else {
                     chosen = __ldg(p.fixed + dev::lds_l(c_tw(1)) + task);

@@ -48,7 +48,9 @@ class lmx_params(ctypes.Structure):
                 ("sigma_floor", ctypes.c_double), ("lc0", ctypes.c_double), ("alpha", ctypes.c_double),
                 ("mem_enable", ctypes.c_int32), ("mem_pad", ctypes.c_int32), ("mem_cap", ctypes.c_int64),
                 ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double),
-                ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double)]
+                ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double),
+                ("sep_dynamic", ctypes.c_int32), ("sep_pad", ctypes.c_int32), ("dyn_rate", ctypes.c_double),
+                ("dyn_window", ctypes.c_double)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version",
@@ -146,12 +148,17 @@ class Params:
     # Separate's checkpoint synchronisation (lmx_params.sync_*); 0 = co-located proxy
     sync_interval: int = 0
     sync_latency: float = 0.0
+    # SeparateDynamic (lmx_params.sep_dynamic / dyn_rate / dyn_window)
+    sep_dynamic: int = 0
+    dyn_rate: float = 50.0
+    dyn_window: float = 10.0
 
     def c(self) -> lmx_params:
         return lmx_params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1, self.lambda2,
                           self.tau, self.slo_mult, self.slo_const, self.sigma_floor, self.lc0, self.alpha,
                           self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax, self.mem_pen,
-                          self.sync_interval, 0, self.sync_latency)
+                          self.sync_interval, 0, self.sync_latency, self.sep_dynamic, 0, self.dyn_rate,
+                          self.dyn_window)
 
 
 class Context:

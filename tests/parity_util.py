@@ -18,7 +18,8 @@ def oracle_params(lp) -> oracle.OracleParams:
                                deprioritize=lp.deprioritize, slo_mode=lp.slo_mode, qcap=lp.qcap,
                                slo_const=lp.slo_const, mem_enable=lp.mem_enable, mem_cap=lp.mem_cap,
                                mem_dt=lp.mem_dt, mem_tmax=lp.mem_tmax, mem_pen=lp.mem_pen,
-                               sync_interval=lp.sync_interval, sync_latency=lp.sync_latency)
+                               sync_interval=lp.sync_interval, sync_latency=lp.sync_latency,
+                               sep_dynamic=lp.sep_dynamic, dyn_rate=lp.dyn_rate, dyn_window=lp.dyn_window)
 
 
 def rel_err(a, b):

@@ -61,7 +61,7 @@ def test_struct_layouts_match_header():
     from paper_2507_21276_b200 import lemix
     assert lemix.SUMMARY_DTYPE.itemsize == 8 * 17
     assert lemix.CELL_DTYPE.itemsize == 8 * 16
-    assert ctypes.sizeof(lemix.lmx_params) == 4 * 4 + 8 * 8 + 4 * 2 + 8 * 4 + 4 * 2 + 8
+    assert ctypes.sizeof(lemix.lmx_params) == 4 * 4 + 8 * 8 + 4 * 2 + 8 * 4 + 4 * 2 + 8 + 4 * 2 + 8 * 2
     assert ctypes.sizeof(lemix.lmx_traces) == 8 * 6
 
 

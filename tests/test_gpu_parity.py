@@ -148,3 +148,15 @@ def test_separate_checkpoint_sync(interval, latency):
     tr = workload.concat(parts)
     g, osum, _ = check(4, 2, tr, P(policy=lemix.LMX_SEPARATE, sync_interval=interval, sync_latency=latency))
     assert (osum["sum_version"] > 0).any() or interval == 100
+
+
+@pytest.mark.parametrize("rate,window", [(0.0, 5.0), (30.0, 2.0), (50.0, 10.0), (80.0, 1.0), (1e30, 3.0)])
+def test_separate_dynamic(rate, window):
+    """SeparateDynamic (DESIGN.md R-sepdyn) bit-exact against the
+    oracle across rates that cross the threshold."""
+    parts = [workload.generate(workload.sweep_spec(r), 6, seed_base=700 + 6 * k)
+             for k, r in enumerate((20.0, 40.0, 60.0, 100.0, 160.0))]
+    tr = workload.concat(parts)
+    check(4, 2, tr, P(policy=lemix.LMX_SEPARATE, sep_dynamic=1, dyn_rate=rate, dyn_window=window))
+    check(8, 2, tr, P(policy=lemix.LMX_SEPARATE, sep_dynamic=1, dyn_rate=rate, dyn_window=window,
+                      sync_interval=7, sync_latency=0.5))
