@@ -504,7 +504,18 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
 
                 // ---- a8: arg-best over the tile: highest f, then lowest node index ----
                 int best;
-                if (LEMIX) {
+                if (LEMIX && NPL == 1) {
+                    // one node per lane (node = tile lane): the tile max of f by a
+                    // butterfly, then the lowest lane holding it (a ballot) -- the
+                    // same total order (f desc, node asc; +0 == -0, no NaN: R > 0)
+                    const bool valid = n_best != INT_MAX;
+                    double fm = valid ? f_best : -kInf;
+#pragma unroll
+                    for (int off = T >> 1; off > 0; off >>= 1) fm = dev::dmax(fm, dev::shfl_xor_w(fm, off, T));
+                    const unsigned hit = __ballot_sync(0xffffffffu, valid && f_best == fm);
+                    const unsigned seg = (hit >> tbase) & (T == 32 ? 0xffffffffu : ((1u << T) - 1u));
+                    best = seg ? __ffs(seg) - 1 : INT_MAX;
+                } else if (LEMIX) {
 #pragma unroll
                     for (int off = T >> 1; off > 0; off >>= 1) {
                         const double f2 = dev::shfl_xor_w(f_best, off, T);
