@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
         dev::opaque(ws[jj]);   // keep in a register: no per-iteration rematerialisation
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
         rbe[jj] = p.ring_be + rbase * ring_words(S, MEM);
+        dev::opaque_ptr(rbe[jj]);
     }
     // commit-only per-node state in shared memory ("cold" words, 8 bytes each,
     // [word][thread] so each thread owns a conflict-free column): per slot jj
