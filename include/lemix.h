@@ -228,6 +228,8 @@ lmx_status lmx_sync(lmx_ctx *ctx);
  * (bits 0-15) | Eq. 4 deferral count saturated at 0xFFFF (bits 16-31);
  * decision_idx = the decision (0-based, per trace) that placed the task;
  * completion = inference end_f^S, training end_b^1; start_f1 = start_f^1.
+ * Tasks a failed trace never decided read node_defer 0xFFFFFFFF,
+ * decision_idx -1 and NaN times (the trace's status says why).
  * Any pointer may be NULL.  `mem` says where the destination lives. */
 lmx_status lmx_get_assignments(lmx_ctx *ctx, uint32_t *node_defer, int32_t *decision_idx, lmx_mem mem);
 lmx_status lmx_get_times(lmx_ctx *ctx, double *completion, double *start_f1, lmx_mem mem);

@@ -613,6 +613,15 @@ lmx_status lmx_run(lmx_ctx *c)
         k.decision_idx = (int32_t *)c->decision_idx.p;
         k.completion = (double *)c->completion.p;
         k.start_f1 = (double *)c->start_f1.p;
+        // tasks a failed trace never decides keep defined sentinels (node/defer
+        // all ones, decision -1, NaN times) instead of stale memory
+        if (M > 0) {
+            lmx_status s0 = c->cuda(cudaMemsetAsync(c->node_defer.p, 0xFF, M * 4, c->stream), "output init");
+            if (s0 == LMX_OK) s0 = c->cuda(cudaMemsetAsync(c->decision_idx.p, 0xFF, M * 4, c->stream), "output init");
+            if (s0 == LMX_OK) s0 = c->cuda(cudaMemsetAsync(c->completion.p, 0xFF, M * 8, c->stream), "output init");
+            if (s0 == LMX_OK) s0 = c->cuda(cudaMemsetAsync(c->start_f1.p, 0xFF, M * 8, c->stream), "output init");
+            if (s0 != LMX_OK) return s0;
+        }
     }
     k.summaries = (lmx_summary *)c->summaries.p;
     k.trace_err = (int64_t *)c->trace_err.p;

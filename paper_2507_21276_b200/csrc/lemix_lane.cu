@@ -493,6 +493,7 @@ __global__ void __launch_bounds__(kLaneBlock, LMX_LANE_MINB) lane_loop_kernel(co
         sm.n_train = nT;
         sm.status = status;
         sm.n_slo_met = sm.n_deferrals = sm.active_nodes = sm.sum_version = 0;
+        sm.n_mem_wait = sm.n_offload = 0;   // (Algorithm 2 runs on the tile kernel only)
         sm.makespan = sm.throughput = sm.sum_ttft = sm.mean_ttft = sm.slo_attainment = 0.0;
         sm.mean_util = sm.mean_len_std = 0.0;
         if (status == LMX_OK) {
