@@ -116,3 +116,28 @@ def test_memory_params_validated():
         kw = dict(mem_enable=1, mem_cap=10, mem_dt=0.1, mem_tmax=1.0, mem_pen=0.0) | bad
         o = oracle.run_trace(ef, eb, 1, 1, tr.arrival, tr.lbk, tr.n_inf[0], oracle.OracleParams(**kw))
         assert o["status"] == oracle.EINVAL, bad
+
+
+def test_without_algorithm2_the_cap_is_exceeded():
+    """SPEC.md:550 (acceptance 6, the PAPER.md:1081 "w/o memory" ablation): on
+    a saturating workload, unlimited admission checked post hoc against the
+    cap has violating admissions, while Algorithm 2 has none
+    (test_admissions_respect_the_cap)."""
+    cap = 600
+    tr = workload.generate(workload.sweep_spec(160.0, tasks=400), 2, seed_base=7 + cap)
+    outs, ef, eb = _run(4, 2, tr)                      # memory model off
+    violations = 0
+    for t, o in enumerate(outs):
+        sub = tr.subset(np.array([t]))
+        nI = int(sub.n_inf[0])
+        lbk = sub.lbk
+        tok = ((lbk >> 12) & 0xFF).astype(np.int64) * (lbk & 0xFFF).astype(np.int64)
+        P = o["paths"]
+        for n in range(4):
+            on = np.nonzero(o["node"] == n)[0]
+            for s in range(2):
+                for x in on:
+                    t0 = P[x, s, 0]
+                    held = sum(tok[q] for q in on if q >= nI and q != x and P[q, s, 0] <= t0 < P[q, s, 3])
+                    violations += held + tok[x] > cap
+    assert violations > 0
