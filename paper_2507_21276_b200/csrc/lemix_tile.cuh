@@ -1,6 +1,6 @@
 // lemix_tile.cuh -- the tile-of-lanes persistent event-loop kernel template
-// (included by lemix_tile_lemix.cu and lemix_tile_base.cu, one translation
-// unit per policy class so the instantiations compile in parallel).
+// (included by lemix_tile_{lemix,base}{,_mem}.cu, one translation unit per
+// policy class and memory model so the instantiations compile in parallel).
 //
 // K1 profile staging : the fp64 SoA profile table (eta_f, eta_b) is copied
 //                      into shared memory once per CTA with a TMA bulk copy
@@ -13,6 +13,14 @@
 //                      lane commits.  Eq. 4 is a tile min.
 //                      Tiles claim traces from a global counter until none are
 //                      left, so long and short traces balance across SMs.
+//
+// Layout of one lane's state: per-node hot values in registers; commit-only
+// values, rarely used per-trace words and the newest W Q_train entries in
+// shared memory (one conflict-free column per thread); older queue entries in
+// a global ring (spilled on eviction only).  The decision body is executed by
+// every lane of the warp (tiles without a trace ride along with live = false),
+// so its shuffles are full-warp segment shuffles; work that only some tiles
+// or lanes need is predicated on place / lane == owner.
 //
 // Compiled with --fmad=false: see lemix_device.cuh for the fp64 discipline.
 #pragma once
