@@ -634,9 +634,10 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                             for (int s = 0; s < SMAX; ++s)
                                 if (s < S) dev::sts_d(c_busy(jj, s), bz[s]);
                             dev::sts_l(c_ntr(jj), (long long)(unsigned)ntr | ((long long)vp << 32));
-                            if (c_status == LMX_OK) {
+                            {
                                 // cached Eq. 2 statistics (DESIGN.md R-stat), computed
-                                // speculatively above; unused while cnt < 2
+                                // speculatively above; unused while cnt < 2.  (Also on a
+                                // queue overflow: that trace stops, its state is dead.)
                                 cnt[jj]++;
                                 dev::sts_l(c_sl(jj), sl_n[jj]);
                                 dev::sts_l(c_sl2(jj), sl2_n[jj]);
