@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                             c_done = dev::last_of(en_s[jj], S);
                             if (is_train && qn[jj] >= p.qcap) {
                                 c_status = LMX_EQCAP;
+                                c_ver = INT_MIN;   // (a version count is never negative)
                             } else if (is_train) {
                                 // backward planning, stages S..1
                                 double2 bw[SMAX];
@@ -654,7 +655,6 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                         }
                     }
                 }
-                if (c_status != LMX_OK) c_ver = INT_MIN;   // (a version count is never negative)
                 c_done = dev::shfl_w(c_done, osrc, T);
                 c_en0 = dev::shfl_w(c_en0, osrc, T);
                 if (p.node_defer) c_st0 = dev::shfl_w(c_st0, osrc, T);
