@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 if (place && lane == owner) {
 #pragma unroll
                     for (int jj = 0; jj < NPL; ++jj) {
-                        if (jj == jb) {
+                        if (NPL == 1 || jj == jb) {   // (one slot: the owner lane's node)
                             double ef[SMAX], eb[SMAX];
                             prof.node<SMAX>(best, ef, eb);
                             const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qh[jj] + qn[jj]};
