@@ -27,9 +27,14 @@
  *     message naming the offending field, trace and task index.
  *   - Asynchrony: lmx_run enqueues on the context's CUDA stream and returns;
  *     lmx_sync waits and returns the first per-trace error (LMX_OK if none).
- *   - Determinism: outputs are a pure function of (profile, traces, params);
- *     they do not depend on the launch geometry, the GPU count or the order
- *     in which traces are scheduled on the device.
+ *   - Determinism: per-trace outputs, per-trace summaries and the per-cell
+ *     aggregates of one rank are a pure function of (profile, traces, params)
+ *     and the cell map; they do not depend on the launch geometry or the
+ *     order in which traces are scheduled on the device (each cell is folded
+ *     over its own traces in trace order).  After lmx_allreduce_cells the
+ *     integer cell fields are exact, but the fp64 cell sums depend on how the
+ *     traces are split across ranks and on NCCL's reduction order (they agree
+ *     within 1e-12 relative, not bit for bit).
  *   - Not thread-safe: one context per thread / GPU.
  */
 #ifndef LEMIX_H
@@ -149,6 +154,13 @@ typedef struct {
     int32_t sep_pad;       /* zero */
     double dyn_rate;       /* requests/s (50 in the paper) */
     double dyn_window;     /* seconds */
+    /* Stepwise debug output: 0 none (default); 1 keep, for
+     * every decision and every node, Algorithm 1's II and R (PAPER.md:474,
+     * line 20) and Eq. 3's f -- see lmx_get_candidates.
+     * Costs 24·N bytes per task of device memory and the writes.  Any other
+     * value -> LMX_EINVAL. */
+    int32_t debug_level;
+    int32_t debug_pad;     /* zero */
 } lmx_params;
 
 /* Per-trace summary (metrics of PAPER.md:786-790).  For a trace whose status
@@ -233,6 +245,15 @@ lmx_status lmx_sync(lmx_ctx *ctx);
  * Any pointer may be NULL.  `mem` says where the destination lives. */
 lmx_status lmx_get_assignments(lmx_ctx *ctx, uint32_t *node_defer, int32_t *decision_idx, lmx_mem mem);
 lmx_status lmx_get_times(lmx_ctx *ctx, double *completion, double *start_f1, lmx_mem mem);
+
+/* debug_level 1 only: per decision and node, (II, R, f) as three doubles,
+ * [n_tasks][n_nodes][3], row offsets[t] + k = decision k of trace t
+ * (decision k of a trace is its k-th placement; traces have one decision per
+ * task).  LeMix: every node is planned and scored.  RR / Separate / Fixed:
+ * only the chosen node is planned; its f and every other node's row are NaN.
+ * Decisions a failed trace never reached are NaN.  `mem` says where the
+ * destination lives.  LMX_ESTATE unless the last run had debug_level 1. */
+lmx_status lmx_get_candidates(lmx_ctx *ctx, double *cand, lmx_mem mem);
 
 /* Per-trace summaries [n_traces] (host memory). */
 lmx_status lmx_get_summaries(lmx_ctx *ctx, lmx_summary *per_trace);

@@ -509,6 +509,11 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
                     cand[(step * N + n) * 3 + 2] = fa[n];
                 }
             }
+            /* Eq. 3 needs R > 0: a forward too short to move the
+             * clock past a makes f undefined; the trace stops as invalid input */
+            int r_bad = 0;
+            for (int n = 0; n < N; ++n) r_bad |= !(Ra[n] > 0.0);
+            if (r_bad) { status = ORC_EINVAL; break; }
             /* highest f wins; ties -> lowest node index ([R-13]) */
             best = 0;
             for (int n = 1; n < N; ++n)

@@ -73,6 +73,7 @@ const char *field_name(int code)
     case lmx::kErrOrder: return "arrival (inference tasks must be non-decreasing)";
     case lmx::kErrFixed: return "fixed_node (must be in [0, n_nodes))";
     case lmx::kErrSeparateN1: return "policy Separate needs n_nodes >= 2 when both kinds are present";
+    case lmx::kErrResponse: return "profile/arrival: a candidate's response time R <= 0 (Eq. 3 undefined; eta too small for the arrival time)";
     default: return "unknown";
     }
 }
@@ -150,11 +151,14 @@ struct lmx_ctx {
     // cells
     int32_t n_cells = 1;
     DevBuf cell_of, cell_i, cell_f;
+    DevBuf cell_start, cell_order;   // CSR of the traces of each cell (lmx_set_cells)
     bool cells_set = false;
 
     // outputs / state
     int per_task = 1;
     DevBuf node_defer, decision_idx, completion, start_f1;
+    DevBuf cand;           // debug_level 1: (II, R, f) per decision and node
+    bool cand_valid = false;
     DevBuf ck;             // Separate's checkpoint lists (sync model)
     DevBuf cell_par;       // per-cell (lambda1, lambda2, tau)
     int32_t n_cell_par = 0;
@@ -207,6 +211,8 @@ void lmx_params_default(lmx_params *p)
     p->sep_pad = 0;
     p->dyn_rate = 50.0;
     p->dyn_window = 10.0;
+    p->debug_level = 0;
+    p->debug_pad = 0;
 }
 
 lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
@@ -398,6 +404,7 @@ lmx_status lmx_set_params(lmx_ctx *c, const lmx_params *p)
         return c->fail(LMX_EINVAL, "params.dyn_rate must be finite and >= 0");
     if (p->sep_dynamic && !(p->dyn_window > 0.0 && std::isfinite(p->dyn_window)))
         return c->fail(LMX_EINVAL, "params.dyn_window must be finite and > 0");
+    if (p->debug_level != 0 && p->debug_level != 1) return c->fail(LMX_EINVAL, "params.debug_level must be 0 or 1");
     if (p->mem_enable) {   // Algorithm 2: Delta_t > 0 and a finite T_max bound the wait loop
         if (p->mem_cap < 0) return c->fail(LMX_EINVAL, "params.mem_cap must be >= 0");
         if (!(p->mem_dt > 0.0 && std::isfinite(p->mem_dt))) return c->fail(LMX_EINVAL, "params.mem_dt must be finite and > 0");
@@ -425,10 +432,27 @@ lmx_status lmx_set_cells(lmx_ctx *c, const int32_t *cell_of, int32_t n_cells)
     for (int64_t t = 0; t < c->n_traces; ++t)
         if (cell_of[t] < 0 || cell_of[t] >= n_cells)
             return c->fail(LMX_EINVAL, "cell_of_trace[" + std::to_string(t) + "] out of range");
+    // per-cell CSR: a counting sort of the traces by cell (stable), so the
+    // reduction visits each cell's traces only, in trace order
+    std::vector<int64_t> start((size_t)n_cells + 1, 0), order((size_t)std::max<int64_t>(c->n_traces, 1));
+    for (int64_t t = 0; t < c->n_traces; ++t) start[(size_t)cell_of[t] + 1]++;
+    for (int32_t q = 0; q < n_cells; ++q) start[(size_t)q + 1] += start[q];
+    {
+        std::vector<int64_t> fill(start.begin(), start.end() - 1);
+        for (int64_t t = 0; t < c->n_traces; ++t) order[(size_t)fill[(size_t)cell_of[t]]++] = t;
+    }
     cudaSetDevice(c->device);
-    if (c->cell_of.ensure(std::max<int64_t>(c->n_traces, 1) * 4) != cudaSuccess) return c->fail(LMX_ENOMEM, "cells");
+    if (c->cell_of.ensure(std::max<int64_t>(c->n_traces, 1) * 4) != cudaSuccess ||
+        c->cell_start.ensure(start.size() * 8) != cudaSuccess || c->cell_order.ensure(order.size() * 8) != cudaSuccess)
+        return c->fail(LMX_ENOMEM, "cells");
     lmx_status s = c->cuda(cudaMemcpyAsync(c->cell_of.p, cell_of, c->n_traces * 4, cudaMemcpyHostToDevice, c->stream),
                            "cells copy");
+    if (s == LMX_OK)
+        s = c->cuda(cudaMemcpyAsync(c->cell_start.p, start.data(), start.size() * 8, cudaMemcpyHostToDevice, c->stream),
+                    "cells copy");
+    if (s == LMX_OK)
+        s = c->cuda(cudaMemcpyAsync(c->cell_order.p, order.data(), order.size() * 8, cudaMemcpyHostToDevice, c->stream),
+                    "cells copy");
     if (s != LMX_OK) return s;
     s = c->cuda(cudaStreamSynchronize(c->stream), "cells copy");
     if (s != LMX_OK) return s;
@@ -548,36 +572,15 @@ lmx_status lmx_run(lmx_ctx *c)
     k.fixed = c->has_fixed ? (const int32_t *)c->fixed.p : nullptr;
     k.eta = (const double *)c->eta.p;
 
-    // kernel variant: the tile-of-lanes kernel by default; the lane-per-trace
-    // variant (small clusters only) with LMX_KERNEL=lane
-    bool lane = false;
-    if (const char *force = getenv("LMX_KERNEL")) {
-        if (!strcmp(force, "lane")) {
-            if (!lmx::lane_supported(c->N, c->S))
-                return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: not supported for this N x S");
-            if (P.mem_enable)
-                return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: the memory model (Algorithm 2) runs on the tile kernel only");
-            if (c->n_cell_par > 0)
-                return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: per-cell parameters run on the tile kernel only");
-            lane = true;
-        }
-    }
-    if (lane) {
-        k.T = 1;
-        k.log2T = 0;
-        k.npl = c->N;
-        k.npad = lmx::lane_nodes_bucket(c->N);
-    }
-
     // geometry: persistent grid = resident CTAs, capped by the number of traces
     int occ_err = 0;
-    const int per_sm = lane ? lmx::lane_occupancy(k, &occ_err) : lmx::event_loop_occupancy(k, &occ_err);
+    const int per_sm = lmx::event_loop_occupancy(k, &occ_err);
     if (occ_err != 0 || per_sm < 1)
         return c->fail(LMX_ECUDA, std::string("event loop occupancy query failed: ") +
                                       cudaGetErrorString((cudaError_t)occ_err));
     int n_sm = 0;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
-    const int block = lane ? lmx::lane_block_threads() : lmx::event_loop_block_threads();
+    const int block = lmx::event_loop_block_threads();
     const int tiles_per_block = block / k.T;
     int64_t grid = (int64_t)n_sm * per_sm;
     const int64_t need = (T + tiles_per_block - 1) / tiles_per_block;
@@ -623,6 +626,15 @@ lmx_status lmx_run(lmx_ctx *c)
             if (s0 != LMX_OK) return s0;
         }
     }
+    c->cand_valid = false;
+    if (P.debug_level == 1) {
+        const size_t nc = (size_t)std::max<int64_t>(M, 1) * c->N * 3;
+        if (c->cand.ensure(nc * 8) != cudaSuccess) return c->fail(LMX_ENOMEM, "debug candidate output allocation");
+        lmx_status s0 = c->cuda(cudaMemsetAsync(c->cand.p, 0xFF, nc * 8, c->stream), "debug output init");
+        if (s0 != LMX_OK) return s0;
+        k.cand = (double *)c->cand.p;
+        c->cand_valid = true;
+    }
     k.summaries = (lmx_summary *)c->summaries.p;
     k.trace_err = (int64_t *)c->trace_err.p;
     k.work = (unsigned long long *)c->work.p;
@@ -655,19 +667,12 @@ lmx_status lmx_run(lmx_ctx *c)
         cudaEventRecord(c->ev_armed, c->stream);
         k.ready = (const unsigned *)c->ready.p;
         k.chunk_tasks = chunk;
-    }
-    c->launches = 0;
-    cudaEventRecord(c->ev0, c->stream);
-    if (T > 0) {
-        int e = lane ? lmx::launch_lane_loop(k, (int)grid, c->stream)
-                     : lmx::launch_event_loop(k, (int)grid, c->stream);
-        if (e != 0) return c->cuda((cudaError_t)e, "event loop launch");
-        c->launches++;
-    }
-    cudaEventRecord(c->ev1, c->stream);
-    if (stream_in) {
-        // the copies run on a non-blocking stream while the kernel consumes
-        // the chunks that have landed; the context stream then waits for them
+        // Every copy is enqueued BEFORE the kernel that waits on them: the
+        // copies run on a non-blocking stream while the kernel consumes the
+        // chunks that have landed, and an execution that serialises the two
+        // streams (ncu kernel replay, CUDA_DEVICE_MAX_CONNECTIONS=1) runs the
+        // copies first instead of spinning forever.  A failed enqueue returns
+        // here, before anything waits on the flag.
         cudaStreamWaitEvent(c->copy_stream, c->ev_armed, 0);
         for (int64_t q = 0; q < n_chunks && s == LMX_OK; ++q) {
             const int64_t b = q * chunk, e = std::min(M, b + chunk);
@@ -680,16 +685,34 @@ lmx_status lmx_run(lmx_ctx *c)
                 s = c->cuda(cudaMemcpyAsync(c->ready.p, c->h_seq + q, 4, cudaMemcpyHostToDevice, c->copy_stream),
                             "ready flag");
         }
+        if (s != LMX_OK) {
+            cudaStreamSynchronize(c->copy_stream);
+            return s;
+        }
         cudaEventRecord(c->ev_copied, c->copy_stream);
+    }
+    c->launches = 0;
+    cudaEventRecord(c->ev0, c->stream);
+    if (T > 0) {
+        int e = lmx::launch_event_loop(k, (int)grid, c->stream);
+        if (e != 0) {
+            if (stream_in) cudaStreamSynchronize(c->copy_stream);
+            return c->cuda((cudaError_t)e, "event loop launch");
+        }
+        c->launches++;
+    }
+    cudaEventRecord(c->ev1, c->stream);
+    if (stream_in) {
+        // the context stream (cell reduction, later runs) waits for the copies
         cudaStreamWaitEvent(c->stream, c->ev_copied, 0);
-        if (s != LMX_OK) return s;
         c->host_pending = false;   // the data now lives in the context's buffers
     }
 
     lmx::CellParams cp{};
     cp.n_traces = T;
     cp.n_cells = c->n_cells;
-    cp.cell_of = c->cells_set ? (const int32_t *)c->cell_of.p : nullptr;
+    cp.cell_start = c->cells_set ? (const int64_t *)c->cell_start.p : nullptr;
+    cp.order = c->cells_set ? (const int64_t *)c->cell_order.p : nullptr;
     cp.summaries = (const lmx_summary *)c->summaries.p;
     cp.cell_i = (int64_t *)c->cell_i.p;
     cp.cell_f = (double *)c->cell_f.p;
@@ -701,7 +724,7 @@ lmx_status lmx_run(lmx_ctx *c)
     c->grid = (int32_t)grid;
     c->block = block;
     c->lanes = k.T;
-    c->smem = lane ? lmx::lane_smem_bytes(k) : lmx::event_loop_smem_bytes(k);
+    c->smem = lmx::event_loop_smem_bytes(k);
     c->ran = true;
     c->synced = false;
     return LMX_OK;
@@ -765,6 +788,15 @@ lmx_status lmx_get_times(lmx_ctx *c, double *completion, double *start_f1, lmx_m
     lmx_status s = copy_out(c, completion, c->completion, c->n_tasks * 8, mem, "completion copy");
     if (s == LMX_OK) s = copy_out(c, start_f1, c->start_f1, c->n_tasks * 8, mem, "start_f1 copy");
     return s;
+}
+
+lmx_status lmx_get_candidates(lmx_ctx *c, double *cand, lmx_mem mem)
+{
+    if (!c) return LMX_EINVAL;
+    if (!c->ran || !c->synced) return c->fail(LMX_ESTATE, "lmx_get_candidates: run and sync first");
+    if (!c->cand_valid) return c->fail(LMX_ESTATE, "lmx_get_candidates: the last run had debug_level 0");
+    cudaSetDevice(c->device);
+    return copy_out(c, cand, c->cand, (size_t)c->n_tasks * c->N * 3 * 8, mem, "candidate copy");
 }
 
 lmx_status lmx_get_summaries(lmx_ctx *c, lmx_summary *per_trace)

@@ -58,6 +58,7 @@ struct KParams {
     int32_t *decision_idx;
     double *completion;
     double *start_f1;
+    double *cand;              // debug_level 1: [n_tasks * N][3] (II, R, f) per decision and node, or nullptr
 
     lmx_summary *summaries;    // device [n_traces]
     int64_t *trace_err;        // device [n_traces]: (task << 8) | field code, -1 none
@@ -71,13 +72,14 @@ struct KParams {
 // field codes for trace_err (reported by lmx_last_error)
 enum : int32_t {
     kErrNone = 0, kErrLen = 1, kErrBatch = 2, kErrKind = 3, kErrBits = 4, kErrArrival = 5,
-    kErrOrder = 6, kErrFixed = 7, kErrSeparateN1 = 8
+    kErrOrder = 6, kErrFixed = 7, kErrSeparateN1 = 8, kErrResponse = 9
 };
 
 struct CellParams {
     int64_t n_traces;
     int32_t n_cells;
-    const int32_t *cell_of;    // device [n_traces] or nullptr (all in cell 0)
+    const int64_t *cell_start; // device [n_cells+1] CSR over `order`, or nullptr (one cell: all traces)
+    const int64_t *order;      // device [n_traces]: trace indices sorted (stably) by cell
     const lmx_summary *summaries;
     int64_t *cell_i;           // [n_cells][LMX_CELL_NI]
     double *cell_f;            // [n_cells][LMX_CELL_NF]
@@ -92,13 +94,5 @@ int event_loop_block_threads();
 int event_loop_occupancy(const KParams &p, int *err);
 int launch_event_loop(const KParams &p, int grid, void *stream);
 int launch_cells(const CellParams &c, void *stream);
-
-// lane-per-trace variant (lemix_lane.cu): N <= 8, S <= 4, N*S small
-bool lane_supported(int N, int S);
-int lane_smem_bytes(const KParams &p);
-int lane_block_threads();
-int lane_nodes_bucket(int N);
-int lane_occupancy(const KParams &p, int *err);
-int launch_lane_loop(const KParams &p, int grid, void *stream);
 
 }  // namespace lmx

@@ -48,9 +48,12 @@ __global__ void __launch_bounds__(kCellBlock) cells_kernel(const CellParams c)
     for (int k = 0; k < LMX_CELL_NI; ++k) ai[k] = 0;
 #pragma unroll
     for (int k = 0; k < LMX_CELL_NF; ++k) af[k] = 0.0;
-    for (long long t = threadIdx.x; t < c.n_traces; t += kCellBlock) {
-        const int ct = c.cell_of ? c.cell_of[t] : 0;
-        if (ct != cell) continue;
+    // the cell's traces only (a CSR over traces sorted by cell, built on the
+    // host), in a fixed order: thread k folds members k, k + 256, ...
+    const long long b = c.cell_start ? c.cell_start[cell] : 0;
+    const long long e = c.cell_start ? c.cell_start[cell + 1] : c.n_traces;
+    for (long long m = b + threadIdx.x; m < e; m += kCellBlock) {
+        const long long t = c.order ? c.order[m] : m;
         const lmx_summary s = c.summaries[t];
         ai[0] += 1;
         if (s.status != LMX_OK) { ai[1] += 1; continue; }

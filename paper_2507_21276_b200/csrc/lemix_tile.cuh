@@ -442,6 +442,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 double st0_s[NPL];
                 double f_best = 0.0;
                 int n_best = INT_MAX;
+                bool r_bad = false;   // a candidate with R <= 0 (Eq. 3 undefined)
                 // Eq. 2 statistics of each owned node if this task is committed
                 // there (DESIGN.md R-stat), computed here by every lane -- where
                 // the work overlaps the other candidates' latency -- instead of
@@ -492,7 +493,13 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                             const double tau = cpar ? dev::lds_d(c_tw(6)) : p.tau;
                             const double IP = -dev::dmax(IIS - (a - a_last), tau);        // Eq. 1
                             const double f = (IP + lam2 * LC) / (lam1 * R);               // Eq. 3
+                            r_bad |= !(R > 0.0);
                             if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
+                            if (p.cand)   // debug_level 1: this candidate's (II, R, f) (uniform branch)
+                                dev::put_cand(p.cand, (dev::lds_l(c_tw(1)) + step) * N + n, II, R, f);
+                        } else if (p.cand) {
+                            dev::put_cand(p.cand, (dev::lds_l(c_tw(1)) + step) * N + n, II,
+                                          dev::last_of(en_s[jj], S) - a, __longlong_as_double(-1ll));
                         }
                         {   // speculative statistics: count cnt+1, sums + l, + l^2
                             const long long c = cnt[jj] + 1;
@@ -511,6 +518,20 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                     }
                 }
 
+                // R <= 0 (a forward too short to advance the clock): the trace
+                // stops with LMX_EINVAL before anything is committed, as in the oracle
+                bool place_c = place;
+                if (LEMIX) {
+                    const unsigned rb = __ballot_sync(0xffffffffu, r_bad);
+                    if ((rb >> tbase) & (T == 32 ? 0xffffffffu : ((1u << T) - 1u))) {
+                        if (place) {
+                            status = LMX_EINVAL;
+                            if (tl == 0) dev::sts_l(c_tw(3), ((long long)task << 8) | kErrResponse);
+                        }
+                        place_c = false;
+                    }
+                }
+
                 // ---- a8: arg-best over the tile: highest f, then lowest node index ----
                 int best;
                 if (LEMIX && NPL == 1) {
@@ -523,7 +544,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                     for (int off = T >> 1; off > 0; off >>= 1) fm = dev::dmax(fm, dev::shfl_xor_w(fm, off, T));
                     const unsigned hit = __ballot_sync(0xffffffffu, valid && f_best == fm);
                     const unsigned seg = (hit >> tbase) & (T == 32 ? 0xffffffffu : ((1u << T) - 1u));
-                    best = seg ? __ffs(seg) - 1 : INT_MAX;
+                    best = seg ? __ffs(seg) - 1 : 0;   // (empty only off the live path)
                 } else if (LEMIX) {
 #pragma unroll
                     for (int off = T >> 1; off > 0; off >>= 1) {
@@ -546,7 +567,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 const int jb = best >> log2T;
                 double c_done = 0.0, c_en0 = 0.0, c_st0 = 0.0;
                 int c_ver = 0, c_status = LMX_OK, c_mem = 0;
-                if (place && lane == owner) {
+                if (place_c && lane == owner) {
 #pragma unroll
                     for (int jj = 0; jj < NPL; ++jj) {
                         if (NPL == 1 || jj == jb) {   // (one slot: the owner lane's node)
@@ -661,9 +682,9 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 c_ver = __shfl_sync(0xffffffffu, c_ver, osrc, T);
                 if (MEM) {
                     c_mem = __shfl_sync(0xffffffffu, c_mem, osrc, T);
-                    if (place && c_ver != INT_MIN) { n_mwait += c_mem & 0xff; n_moff += c_mem >> 8; }
+                    if (place_c && c_ver != INT_MIN) { n_mwait += c_mem & 0xff; n_moff += c_mem >> 8; }
                 }
-                if (!place) {
+                if (!place_c) {
                 } else if (c_ver == INT_MIN) {
                     status = LMX_EQCAP;
                 } else {

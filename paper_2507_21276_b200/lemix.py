@@ -25,7 +25,7 @@ STATUS_NAMES = {0: "LMX_OK", 1: "LMX_EINVAL", 2: "LMX_ESTATE", 3: "LMX_ENOMEM", 
 
 EXPORTS = ("lmx_params_default", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_load_profile",
            "lmx_load_traces", "lmx_set_params", "lmx_set_cells", "lmx_set_cell_params", "lmx_set_outputs", "lmx_run", "lmx_sync",
-           "lmx_get_assignments", "lmx_get_times", "lmx_get_summaries", "lmx_get_cells",
+           "lmx_get_assignments", "lmx_get_times", "lmx_get_candidates", "lmx_get_summaries", "lmx_get_cells",
            "lmx_allreduce_cells", "lmx_nccl_unique_id", "lmx_nccl_comm_init", "lmx_nccl_comm_destroy",
            "lmx_get_timing", "lmx_get_geometry")
 
@@ -50,7 +50,7 @@ class lmx_params(ctypes.Structure):
                 ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double),
                 ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double),
                 ("sep_dynamic", ctypes.c_int32), ("sep_pad", ctypes.c_int32), ("dyn_rate", ctypes.c_double),
-                ("dyn_window", ctypes.c_double)]
+                ("dyn_window", ctypes.c_double), ("debug_level", ctypes.c_int32), ("debug_pad", ctypes.c_int32)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version",
@@ -91,6 +91,7 @@ def load_library():
         "lmx_sync": (st, [vp]),
         "lmx_get_assignments": (st, [vp, vp, vp, ctypes.c_int]),
         "lmx_get_times": (st, [vp, vp, vp, ctypes.c_int]),
+        "lmx_get_candidates": (st, [vp, vp, ctypes.c_int]),
         "lmx_get_summaries": (st, [vp, vp]),
         "lmx_get_cells": (st, [vp, vp]),
         "lmx_allreduce_cells": (st, [vp, vp]),
@@ -152,13 +153,15 @@ class Params:
     sep_dynamic: int = 0
     dyn_rate: float = 50.0
     dyn_window: float = 10.0
+    # stepwise debug output (lmx_params.debug_level): 1 = (II, R, f) per decision and node
+    debug_level: int = 0
 
     def c(self) -> lmx_params:
         return lmx_params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1, self.lambda2,
                           self.tau, self.slo_mult, self.slo_const, self.sigma_floor, self.lc0, self.alpha,
                           self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax, self.mem_pen,
                           self.sync_interval, 0, self.sync_latency, self.sep_dynamic, 0, self.dyn_rate,
-                          self.dyn_window)
+                          self.dyn_window, self.debug_level, 0)
 
 
 class Context:
@@ -236,6 +239,9 @@ class Context:
     def lmx_get_times(self, completion=None, start_f1=None, mem=LMX_HOST):
         return self._check(self.lib.lmx_get_times(self.h, _ptr(completion), _ptr(start_f1), mem))
 
+    def lmx_get_candidates(self, cand, mem=LMX_HOST):
+        return self._check(self.lib.lmx_get_candidates(self.h, _ptr(cand), mem))
+
     def lmx_get_summaries(self, n_traces):
         out = np.zeros(n_traces, SUMMARY_DTYPE)
         self._check(self.lib.lmx_get_summaries(self.h, out.ctypes.data))
@@ -292,6 +298,7 @@ class RunResult:
     decision_idx: np.ndarray | None = None
     completion: np.ndarray | None = None
     start_f1: np.ndarray | None = None
+    cand: np.ndarray | None = None
     kernel_ms: float = 0.0
     run_ms: float = 0.0
     launches: int = 0
@@ -334,6 +341,9 @@ def run(eta_f, eta_b, n_nodes, n_stages, traces, params: Params | None = None, d
             res.start_f1 = np.zeros(m, np.float64)
             ctx.lmx_get_assignments(res.node_defer, res.decision_idx)
             ctx.lmx_get_times(res.completion, res.start_f1)
+        if params.debug_level == 1:
+            res.cand = np.zeros((traces.n_tasks, n_nodes, 3), np.float64)
+            ctx.lmx_get_candidates(res.cand)
         res.kernel_ms, res.run_ms, res.launches = ctx.lmx_get_timing()
         return res
     finally:

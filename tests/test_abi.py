@@ -57,12 +57,31 @@ def test_params_default_without_gpu(lib):
     assert p.policy == 0 and p.lambda1 == 1.0 and p.slo_mult == 5.0 and p.qcap == 512
 
 
-def test_struct_layouts_match_header():
+def test_struct_layouts_match_header(tmp_path):
+    """Every field offset and struct size of the ctypes mirrors equals the C
+    compiler's for include/lemix.h (a C probe compiled here)."""
+    import subprocess
     from paper_2507_21276_b200 import lemix
-    assert lemix.SUMMARY_DTYPE.itemsize == 8 * 17
-    assert lemix.CELL_DTYPE.itemsize == 8 * 16
-    assert ctypes.sizeof(lemix.lmx_params) == 4 * 4 + 8 * 8 + 4 * 2 + 8 * 4 + 4 * 2 + 8 + 4 * 2 + 8 * 2
-    assert ctypes.sizeof(lemix.lmx_traces) == 8 * 6
+    structs = {"lmx_params": lemix.lmx_params, "lmx_traces": lemix.lmx_traces, "lmx_profile": lemix.lmx_profile}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "lemix.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
+        for fname, _ in cls._fields_:
+            lines.append(f'printf("{name}.{fname} %zu\\n", offsetof({name}, {fname}));')
+    lines += ['printf("lmx_summary %zu\\n", sizeof(lmx_summary));',
+              'printf("lmx_cell_summary %zu\\n", sizeof(lmx_cell_summary));', "return 0; }"]
+    src = tmp_path / "probe.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "probe"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    got = dict(l.split() for l in subprocess.run([str(exe)], capture_output=True, text=True, check=True)
+               .stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got[name]) == ctypes.sizeof(cls), name
+        for fname, _ in cls._fields_:
+            assert int(got[f"{name}.{fname}"]) == getattr(cls, fname).offset, (name, fname)
+    assert int(got["lmx_summary"]) == lemix.SUMMARY_DTYPE.itemsize
+    assert int(got["lmx_cell_summary"]) == lemix.CELL_DTYPE.itemsize
 
 
 def test_no_gpu_fails_loudly():

@@ -19,29 +19,6 @@ def P(**kw):
     return lemix.Params(**kw)
 
 
-@pytest.fixture(autouse=True, params=["tile", "lane"])
-def kernel_variant(request, monkeypatch):
-    """Run every parity case through both event-loop variants: the default
-    tile-of-lanes kernel and (where N, S allow it) the lane-per-trace kernel."""
-    if request.param == "lane":
-        monkeypatch.setenv("LMX_KERNEL", "lane")
-    else:
-        monkeypatch.delenv("LMX_KERNEL", raising=False)
-    return request.param
-
-
-@pytest.fixture(autouse=True)
-def _skip_unsupported_lane(request, kernel_variant):
-    if kernel_variant != "lane":
-        return
-    shape = request.node.callspec.params if hasattr(request.node, "callspec") else {}
-    N, S = shape.get("N", 4), shape.get("S", 2)
-    if request.node.name.startswith("test_large"):
-        N, S = 64, 8
-    if not ((N <= 4 and S <= 4) or (N <= 8 and S <= 2)):
-        pytest.skip("lane kernel covers N <= 4 with S <= 4, and N <= 8 with S <= 2")
-
-
 POLICIES = [lemix.LMX_LEMIX, lemix.LMX_RR, lemix.LMX_SEPARATE]
 
 

@@ -272,3 +272,16 @@ def test_invalid_inputs_rejected():
                 [(1.0, 10, 1, 0), (0.5, 10, 1, 0)]):
         tr, o = run1(1, 1, 1.0, 1.0, bad)
         assert o["status"] == oracle.EINVAL, bad
+
+
+def test_response_time_zero_is_invalid_input():
+    """Eq. 3 divides by R; R = 0 (a + dF rounds to a) is
+    rejected as invalid input instead of scoring with inf/NaN."""
+    ef, eb = workload.profile(4, 2)
+    tr = workload.from_lists([[(1e10, 1, 1, 0), (0.0, 1, 1, 1)]])
+    o = oracle.run_trace(ef, eb, 4, 2, tr.arrival, tr.lbk, tr.n_inf[0], oracle.OracleParams())
+    assert o["status"] == 1   # ORC_EINVAL
+    # one ulp more room and the same trace is fine: a = 1e9 (ulp 1.2e-7 < dF)
+    tr = workload.from_lists([[(1e9, 1, 1, 0), (0.0, 1, 1, 1)]])
+    o = oracle.run_trace(ef, eb, 4, 2, tr.arrival, tr.lbk, tr.n_inf[0], oracle.OracleParams())
+    assert o["status"] == 0

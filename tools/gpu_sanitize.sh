@@ -17,11 +17,4 @@ PY
 for tool in memcheck racecheck synccheck initcheck; do
   echo "== $tool"
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 9 python /tmp/san.py 2>&1 | tail -4
-  LMX_KERNEL=lane timeout 600 compute-sanitizer --tool $tool --error-exitcode 9 python -c "
-import sys; sys.path.insert(0, '.')
-import workload
-from paper_2507_21276_b200 import lemix
-ef, eb = workload.profile(4, 2)
-tr = workload.generate(workload.tiny_spec(rate=60.0, n_inf=150), 4, seed_base=3)
-print('lane', lemix.run(ef, eb, 4, 2, tr, lemix.Params(), outputs=True).status)" 2>&1 | tail -2
 done
