@@ -17,7 +17,6 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liblemix_oracle.so")
-_lib = None
 
 LEMIX, RR, SEPARATE, FIXED = 0, 1, 2, 3
 OK, EINVAL, EQCAP, EBUDGET = 0, 1, 6, 7
@@ -62,12 +61,19 @@ class Counters(ctypes.Structure):
 SUMMARY_DTYPE = np.dtype([(k, np.int64) for k in SUMMARY_INT] + [(k, np.float64) for k in SUMMARY_F64])
 
 
-def _load():
-    global _lib
-    if _lib is None:
-        if not os.path.exists(_LIB_PATH):
-            raise RuntimeError(f"{_LIB_PATH} missing: run __graft_entry__.build()")
-        lib = ctypes.CDLL(_LIB_PATH)
+_libs = {}
+
+
+def _load(textbook: bool = False):
+    """The oracle library; textbook=True loads the variant built with
+    -DORC_TEXTBOOK (SURVEY.md 8c.4's division / Horner forms of Eq. 2), used
+    only by tests/test_oracle_forms.py."""
+
+    path = _LIB_PATH.replace(".so", "_textbook.so") if textbook else _LIB_PATH
+    if path not in _libs:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} missing: run __graft_entry__.build()")
+        lib = ctypes.CDLL(path)
         vp = ctypes.c_void_p
         lib.orc_run_trace.restype = ctypes.c_int
         lib.orc_run_trace.argtypes = [ctypes.POINTER(Profile), ctypes.POINTER(Params), ctypes.c_int64,
@@ -78,8 +84,8 @@ def _load():
                                       vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(Counters)]
         lib.orc_exp_neg.restype = ctypes.c_double
         lib.orc_exp_neg.argtypes = [ctypes.c_double]
-        _lib = lib
-    return _lib
+        _libs[path] = lib
+    return _libs[path]
 
 
 @dataclass
@@ -122,8 +128,8 @@ def _ptr(a):
     return None if a is None else a.ctypes.data
 
 
-def exp_neg(t: float) -> float:
-    return _load().orc_exp_neg(float(t))
+def exp_neg(t: float, textbook: bool = False) -> float:
+    return _load(textbook).orc_exp_neg(float(t))
 
 
 def run_trace(eta_f, eta_b, n_nodes, n_stages, arrival, lbk, n_inf, params: OracleParams,
@@ -162,10 +168,10 @@ def run_trace(eta_f, eta_b, n_nodes, n_stages, arrival, lbk, n_inf, params: Orac
 
 
 def run_batch(eta_f, eta_b, n_nodes, n_stages, traces, params: OracleParams, fixed_node=None,
-              outputs=True):
+              outputs=True, textbook=False):
     """Run a CSR batch (workload.Traces).  Returns (summaries structured array,
     per-task dict or None, counters dict, first error status)."""
-    lib = _load()
+    lib = _load(textbook)
     eta_f = np.ascontiguousarray(eta_f, np.float64)
     eta_b = np.ascontiguousarray(eta_b, np.float64)
     prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data)

@@ -58,6 +58,18 @@ double orc_exp_neg(double t)
         0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22,
         0x1.ae64567f544e4p-26, 0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};   /* 1/i! */
     if (t > 700.0) return 0.0;
+#ifdef ORC_TEXTBOOK
+    /* SURVEY.md 8c.4 text form (Horner, degree 13), kept only to test that
+     * the Estrin form above [R-exp] changes no scheduling result */
+    {
+        double x = -t;
+        double k = rint(x * 0x1.71547652b82fep0);
+        double r = (x - k * 0x1.62e42fee00000p-1) - k * 0x1.a39ef35793c76p-33;
+        double p = C[13];
+        for (int i = 12; i >= 0; --i) p = p * r + C[i];
+        return ldexp(p, (int)k);
+    }
+#endif
     double x = -t;
     double k = rint(x * 0x1.71547652b82fep0);       /* round half to even */
     double hi = x - k * 0x1.62e42fee00000p-1;      /* ln2 high part */
@@ -215,6 +227,19 @@ static double length_consistency(const trace_t *T, const node_t *nd, int l)
     const orc_params *P = T->par;
     if (nd->hist_cnt < 2) { T->cnt->lc_cold++; return P->lc0; }
     T->cnt->lc_exp++;
+#ifdef ORC_TEXTBOOK
+    /* SURVEY.md 8c.4 text form (true divisions), kept only to test that the
+     * reciprocal form below [R-stat] changes no scheduling result */
+    {
+        double mu = (double)nd->hist_sum / (double)nd->hist_cnt;
+        int64_t var = nd->hist_cnt * nd->hist_sumsq - nd->hist_sum * nd->hist_sum;
+        double sigma = MAX(sqrt((double)var) / (double)nd->hist_cnt, P->sigma_floor);
+        double k = 0.5 / (sigma * sigma);
+        double c = 1.0 / (sigma * 0x1.40d931ff62705p+1);         /* sqrt(2 pi) */
+        double d = (double)l - mu;
+        return c * orc_exp_neg((d * d) * k);
+    }
+#endif
     double inv_c = 1.0 / (double)nd->hist_cnt;
     double mu = (double)nd->hist_sum * inv_c;
     int64_t var_num = nd->hist_cnt * nd->hist_sumsq - nd->hist_sum * nd->hist_sum; /* cnt²·Var, exact */

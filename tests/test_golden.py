@@ -28,6 +28,7 @@ def load(path):
     ef = np.full(N * S, g["eta_f"], np.float64)
     eb = np.full(N * S, g["eta_b"], np.float64)
     tr = from_lists([[tuple(t) for t in g["tasks"]]])
+    g["fixed_np"] = np.asarray(g["fixed"], np.int32) if "fixed" in g else None
     return g, N, S, ef, eb, tr
 
 
@@ -39,7 +40,8 @@ def test_fixture_set_present():
 def test_oracle_matches_golden(path):
     g, N, S, ef, eb, tr = load(path)
     par = oracle.OracleParams(**g["params"])
-    o = oracle.run_trace(ef, eb, N, S, tr.arrival, tr.lbk, tr.n_inf[0], par, want_paths=True, want_cand=True)
+    o = oracle.run_trace(ef, eb, N, S, tr.arrival, tr.lbk, tr.n_inf[0], par, fixed_node=g["fixed_np"],
+                         want_paths=True, want_cand=True)
     assert o["status"] == 0
     ex = g["expect"]
     for task, stages in ex.get("paths", {}).items():
@@ -69,7 +71,8 @@ def test_oracle_matches_golden(path):
 def test_cuda_path_matches_golden(path):
     lemix = pytest.importorskip("paper_2507_21276_b200.lemix")
     g, N, S, ef, eb, tr = load(path)
-    res = lemix.run(ef, eb, N, S, tr, lemix.Params(**g["params"]), device=0, outputs=True)
+    res = lemix.run(ef, eb, N, S, tr, lemix.Params(**g["params"]), device=0, outputs=True,
+                    fixed_node=g["fixed_np"])
     assert res.status == 0, res.error
     ex = g["expect"]
     node = (res.node_defer & 0xFFFF).astype(int)
