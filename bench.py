@@ -2,14 +2,17 @@
 """Benchmark of the LeMix placement step on B200 (BASELINE.json metric:
 scheduling decisions/s and traces/s at 1/2/4/8 GPUs, % of roofline).
 
-Workload (config.workload): the Monte Carlo scaling config -- per GPU 65,536
-independent seeded traces of 10k inference requests + 10k training
-micro-batches (20k decisions each; half Poisson, half bursty Gamma CV = 3
-arrivals, LogNormal lengths), N = 4 nodes x S = 2 stages, Llama-8B profile,
-LeMix policy, summary-only outputs.  One step = one lmx_run over all traces
-(every decision of every trace) + the per-cell summary reduction (+ the NCCL
-all-reduce of the cell aggregates when N > 1).  Weak scaling: each rank owns
-its own 65,536 traces (seeds offset by rank), no data-path collective.
+Workload (config.workload): the Monte Carlo scaling config (BASELINE.json
+configs[4]) -- a fixed set of 65,536 independent seeded traces of 10k
+inference requests + 10k training micro-batches (20k decisions each; half
+Poisson, half bursty Gamma CV = 3 arrivals, LogNormal lengths), N = 4 nodes x
+S = 2 stages, Llama-8B profile, LeMix policy, summary-only outputs.  One step =
+one lmx_run over every trace of the rank (every decision) + the per-cell
+summary reduction (+ the NCCL all-reduce of the cell aggregates when N > 1).
+Strong scaling (default): rank r of P takes traces
+t = r (mod P) of the fixed set (dist.strided_shard), so the job is the same at
+every P; --scaling weak gives every rank its own 65,536 traces instead.  No
+data-path collective either way.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lemix|reference]
 
@@ -35,23 +38,32 @@ N_NODES, N_STAGES = 4, 2
 METRIC = "scheduling decisions/sec"
 UNIT = "decisions/s"
 
-# Algorithmic fp64 operations (IEEE add/sub/mul/div/sqrt/compare) per oracle
-# event, read off the canonical expression sheet.
+# Algorithmic fp64 operations per oracle event, read off the canonical
+# expression sheet (SURVEY.md §8(d) convention): an IEEE
+# add / sub / mul / compare / MAX / MIN / select counts 1; a division, a sqrt
+# and exp_neg count their fixed fp64 instruction expansions on sm_100a
+# (cuobjdump -sass of the kernel, profiles/r02_fp64_expansions.txt): div.rn.f64
+# = MUFU.RCP64H + 7 DFMA + 1 DMUL = 9, sqrt.rn.f64 = MUFU.RSQ64H + 8 DFMA/DMUL
+# = 9, exp_neg = 36 (clamp, 2 scale mul/sub pairs, rint, 26 Estrin mul/add, 2^k
+# scale, cutoff select).
+DIV, SQRT, EXP = 9, 9, 36
 OP_WEIGHTS = {
-    "decisions": 1 + 2 + 1,      # event select compare; t_last MAX + output fold; release/TTFT MAX
+    "decisions": 1 + 1 + 1 + 1,  # event select compare; t_last MAX; release MAX; ready/defer compare
     "stage_iters": 6,            # dF mul, start MAX, end add, II: sub, sub, add
-    "scan_consumed": 4,          # fit compare, MAX, end add, offset compare (+ GC compare at s=0 ~ +0.5)
+    "scan_consumed": 4.5,        # fit compare, MAX, end add, offset compare (+ GC compare at stage 1)
     "scan_break": 1,             # fit compare
     "offset_adds": 2,            # eta_b*w mul, add
-    "alg1_calls": 4 + 4 + 1,     # Eq.1 (div, sub, sub, MAX), Eq.3 (mul, add, mul, div), arg-best compare
-    "lc_exp": 3 + 34 + 1,        # d sub, d*d, *k; exp_neg (cmp, mul, rint, mul, sub, mul, sub, 13x(mul,add), scale); c*
+    "alg1_calls": 1 + 4 + 3 + DIV + 1,   # R sub; Eq. 1 (II/S, gap sub, sub, MAX); Eq. 3 (mul, add, mul, div); arg-best compare
+    "lc_exp": 3 + EXP + 1,       # d sub, d*d, *k; exp_neg; c*
     "commits_train": 3 * N_STAGES + 2 * N_STAGES,   # backward MAX/mul/add per stage; busy += dB
-    "eq4_checks": 3 * N_NODES + 2 * N_STAGES + 3,   # per node add/mul/MIN; tau_R; sub + compare
+    "eq4_checks": 3 * N_NODES + 2 * N_STAGES + 1 + 2,   # per node add/mul/MIN; tau_R; sub + compare
     "version_scan": 1,
 }
-# per-decision commit work independent of the counters: busy += dF (2S), stats (div, sqrt, div, MAX,
-# mul, div, mul, div = 8), inference TTFT/SLO (sub, add, tau_R 2S+1, compare) ~ counted as 2S+4
-COMMIT_OPS = 2 * N_STAGES + 8 + (2 * N_STAGES + 4) // 2
+# per-decision commit work the counters do not itemise: busy += dF (2S); the
+# winner's Eq. 2 statistics (1/cnt div, mu mul, sqrt, mul, MAX, 1/sigma div,
+# k 2 mul, c mul = 2 DIV + SQRT + 6); an inference task's TTFT (sub), fold (add),
+# tau_R (2S + 1) and SLO compare, on about half the decisions
+COMMIT_OPS = 2 * N_STAGES + (2 * DIV + SQRT + 6) + (3 + 2 * N_STAGES + 1) / 2
 
 
 def ops_per_decision(counters: dict) -> float:
@@ -155,6 +167,79 @@ def oracle_sample(traces, n_threads, policy=0, mem=None):
     return sums, counters, dt, len(bounds)
 
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _oracle_worker(args):
+    """One all-cores worker process: its own slice of the MC traces, generated
+    here, run through the oracle after a common start barrier."""
+    idx, n_total, seed_base, n_inf, n_train, mem, barrier = args
+    import oracle
+    import workload
+    sys.path.insert(0, ROOT)
+    tr = workload.mc_traces_subset(idx, n_total, seed_base, n_inf, n_train, n_threads=1, with_out_len=False)
+    ef, eb = workload.profile(N_NODES, N_STAGES)
+    par = oracle.OracleParams(**(mem or {}))
+    barrier.wait()
+    t0 = time.perf_counter()
+    oracle.run_batch(ef, eb, N_NODES, N_STAGES, tr, par, outputs=False)
+    return tr.n_tasks, time.perf_counter() - t0
+
+
+_BARRIER = None
+
+
+def _init_worker(b):
+    global _BARRIER
+    _BARRIER = b
+
+
+def _oracle_worker_g(args):
+    return _oracle_worker(args + (_BARRIER,))
+
+
+def cpu_baseline(args, n_total, single_traces=96, per_core_traces=32):
+    """The oracle as it stands on this host: single-core
+    decisions/s over `single_traces` traces (~2 s), and an all-cores figure
+    from nproc independent processes over disjoint trace slices (same
+    workload, seeds spread over both the Poisson and the bursty half)."""
+    import multiprocessing as mp
+
+    import oracle
+    import workload
+    ncores = os.cpu_count() or 1
+    ef, eb = workload.profile(N_NODES, N_STAGES)
+    one = sample_indices(n_total, single_traces)
+    tr = workload.mc_traces_subset(one, n_total, args.seed, args.n_inf, args.n_train, with_out_len=False)
+    t0 = time.perf_counter()
+    oracle.run_batch(ef, eb, N_NODES, N_STAGES, tr, oracle.OracleParams(**mem_kw(args)), outputs=False)
+    t1 = time.perf_counter() - t0
+    single = tr.n_tasks / t1
+    many = sample_indices(n_total, ncores * per_core_traces)
+    slices = [many[k::ncores] for k in range(ncores)]
+    ctx = mp.get_context("spawn")
+    bar = ctx.Barrier(ncores)
+    with ctx.Pool(ncores, initializer=_init_worker, initargs=(bar,)) as pool:
+        res = pool.map(_oracle_worker_g, [(sl, n_total, args.seed, args.n_inf, args.n_train, mem_kw(args))
+                                          for sl in slices])
+    decisions = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    return {"value": decisions / wall, "unit": UNIT, "cores": ncores, "kind": "oracle",
+            "single_core": {"value": single, "unit": UNIT, "decisions": int(tr.n_tasks), "seconds": round(t1, 2)},
+            "cpu_model": _cpu_model(),
+            "sample": (f"all cores: {ncores} processes x {per_core_traces} traces ({decisions} decisions), "
+                       f"slowest process {wall:.1f} s; single core: {single_traces} traces "
+                       f"({tr.n_tasks} decisions) in {t1:.1f} s; traces drawn from both halves of the mc set")}
+
+
 def sample_indices(n_traces, n):
     """n trace indices, half from each (Poisson / bursty) half."""
     half = n_traces // 2
@@ -163,18 +248,40 @@ def sample_indices(n_traces, n):
     return np.unique(np.concatenate([a, b]))
 
 
+def shard_traces(n_total, rank, world, seed_base, n_inf, n_train, scaling="strong", out=None):
+    """This rank's traces of the MC config: strong = the strided shard
+    t = rank (mod world) of the fixed n_total-trace set; weak = its own
+    n_total traces (seeds offset by rank).  The gloo test uses the same call."""
+    import workload
+    from paper_2507_21276_b200 import dist as ldist
+    if scaling == "weak":
+        return workload.mc_traces(n_total, seed_base=ldist.weak_seed_base(seed_base, rank, n_total), n_inf=n_inf,
+                                  n_train=n_train, out=out, with_out_len=False)
+    idx = ldist.strided_shard(n_total, rank, world)
+    return workload.mc_traces_subset(idx, n_total, seed_base, n_inf, n_train, out=out, with_out_len=False)
+
+
+def traces_on_rank(n_total, rank, world, scaling):
+    if scaling == "weak":
+        return n_total
+    return len(range(rank, n_total, world))
+
+
 def config_dict(args, world):
     per = args.n_inf + args.n_train
-    return {"workload": (f"mc: {args.traces} seeded traces/GPU x {args.n_inf} inference requests + "
+    scope = "traces/GPU" if args.scaling == "weak" else f"traces sharded over {world} GPU(s)"
+    return {"workload": (f"mc: {args.traces} seeded {scope} x {args.n_inf} inference requests + "
                          f"{args.n_train} training micro-batches (half Poisson, half bursty CV=3), "
                          f"LogNormal lengths, N={N_NODES} nodes x S={N_STAGES} stages, Llama-8B profile, "
                          f"LeMix, summary-only"
                          + (f", Algorithm 2 memory model (cap {args.mem_cap} tokens/GPU, dt {MEM_DT} s, "
                             f"T_max {MEM_TMAX} s)" if args.mem_cap else "")),
-            "traces_per_gpu": args.traces, "tasks_per_trace": per, "n_nodes": N_NODES, "n_stages": N_STAGES,
+            "traces_total": args.traces * (world if args.scaling == "weak" else 1),
+            "traces_per_gpu": traces_on_rank(args.traces, 0, world, args.scaling), "tasks_per_trace": per, "n_nodes": N_NODES, "n_stages": N_STAGES,
             "policy": "lemix", "qcap": args.qcap, "mem_cap_tokens": args.mem_cap or None,
             "l2": f"inputs {args.traces * per * 12 / 1e9:.1f} GB/GPU >> 126 MB L2 (no flush needed)",
-            "parallelism": f"dp{world} (independent traces sharded, one NCCL summary all-reduce)"}
+            "parallelism": (f"dp{world}: {'strided shard t = rank mod ' + str(world) + ' of one fixed seed set' if args.scaling == 'strong' else 'own seed set per rank'}"
+                            f", one NCCL summary all-reduce")}
 
 
 def run_reference(args, rank, world):
@@ -202,7 +309,7 @@ def run_reference(args, rank, world):
     sample = f"{n} traces ({n * (args.n_inf + args.n_train)} decisions) of the mc workload per step"
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_dict(args, world),
             "traces_per_s": n / step,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": used, "kind": "oracle", "sample": sample},
@@ -216,7 +323,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="lemix", choices=["lemix", "reference"])
-    ap.add_argument("--traces", type=int, default=65536, help="traces per GPU")
+    ap.add_argument("--traces", type=int, default=65536,
+                    help="traces in the job (strong scaling) or per GPU (weak scaling)")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--n-inf", type=int, default=10000)
     ap.add_argument("--n-train", type=int, default=10000)
     ap.add_argument("--qcap", type=int, default=512)
@@ -257,14 +366,15 @@ def main():
             dist.barrier()
 
     # ---------------- inputs: pinned host memory, then resident in HBM ----------------
-    T = args.traces
+    T = traces_on_rank(args.traces, rank, world, args.scaling)        # this rank's traces
+    T_job = args.traces * (world if args.scaling == "weak" else 1)    # the whole job's
     per = args.n_inf + args.n_train
     M = T * per
     t_gen = time.perf_counter()
     arrival_h = torch.empty(M, dtype=torch.float64, pin_memory=True)
     lbk_h = torch.empty(M, dtype=torch.int32, pin_memory=True)
-    tr = workload.mc_traces(T, seed_base=args.seed + rank * T, n_inf=args.n_inf, n_train=args.n_train,
-                            out=(arrival_h.numpy(), lbk_h.numpy().view(np.uint32)), with_out_len=False)
+    tr = shard_traces(args.traces, rank, world, args.seed, args.n_inf, args.n_train, args.scaling,
+                      out=(arrival_h.numpy(), lbk_h.numpy().view(np.uint32)))
     t_gen = time.perf_counter() - t_gen
     # a dedicated stream: the library launches on it and the CUDA events below
     # are recorded on it
@@ -323,7 +433,7 @@ def main():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     elapsed = float(t_max.item())
     step_s = elapsed / args.steps
-    decisions_per_step = M * world
+    decisions_per_step = T_job * per          # every decision of every rank's traces
     value = decisions_per_step / step_s
     cells = ctx.lmx_get_cells(1)
     sums_gpu = ctx.lmx_get_summaries(T)
@@ -383,9 +493,7 @@ def main():
         same_f = all(np.array_equal(gs[k].view(np.int64), osum[k].view(np.int64)) for k in lemix.SUMMARY_F64)
         parity = {"sampled_traces": int(len(idx)), "integers_exact": bool(same_int), "fp64_bitwise": bool(same_f)}
         if world == 1 and not args.no_cpu:
-            cpu = {"value": sub.n_tasks / dt, "unit": UNIT, "cores": used, "kind": "oracle",
-                   "sample": f"{len(idx)} traces of the same workload ({sub.n_tasks} decisions), "
-                             f"{used} threads over trace slices, {dt:.1f} s wall"}
+            cpu = cpu_baseline(args, args.traces)
         opd = ops_per_decision(counters)
         peaks, peak_src = measured_peaks()
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
@@ -405,7 +513,8 @@ def main():
                     "frac": achieved / peak_tflops, "traffic": traffic,
                     "kernel": f"lmx::tile::event_loop_kernel<2, true, 1, true, 4, {str(bool(args.mem_cap)).lower()}>",
                     "note": (f"fp64 pipe: {opd:.1f} algorithmic fp64 ops/decision (oracle counters x DESIGN.md "
-                             f"weights) x {M} decisions / {k_s * 1e3:.1f} ms mean kernel time; peak = 64 "
+                             f"weights; div/sqrt/exp = their SASS expansions {DIV}/{SQRT}/{EXP}) x {M} decisions / "
+                             f"{k_s * 1e3:.1f} ms mean kernel time; peak = 64 "
                              f"DP lanes/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz ({peak_src} clock); "
                              f"HBM bound {M * 12 / k_s / 1e9:.0f} GB/s of {peaks.get('hbm_gbs')}"),
                     "max_queue_depth_sample": counters["max_qlen"]}
@@ -414,9 +523,9 @@ def main():
         grid, block, lanes, smem = ctx.lmx_get_geometry()
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": config_dict(args, world),
-                "traces_per_s": T * world / step_s,
+                "traces_per_s": T_job / step_s,
                 "kernel_ms_mean": statistics.mean(kernel_ms),
                 "gpu_launches": launches,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": sampler.report(),

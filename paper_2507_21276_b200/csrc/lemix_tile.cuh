@@ -62,7 +62,7 @@ inline int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
 inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN : 0; }
 // 8-byte shared-memory words of commit-only state per node slot and thread
 // (+ 4 words of scoring state when a lane owns several nodes, see SCOLD)
-__host__ __device__ inline int cold_words(int S, bool scold) { return 2 * S + 3 + (scold ? 4 : 0); }
+__host__ __device__ inline int cold_words(int S, bool scold) { return 2 * S + 4 + (scold ? 4 : 0); }
 
 template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, bool MEM>
 __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_MINB) event_loop_kernel(const KParams p)
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     // [word][thread] so each thread owns a conflict-free column): per slot jj
     // LB[s] (last planned backward end), busy[s], sum l, sum l^2, and
     // (training count, version pointer) -- see cold_words()
-    const uint32_t cstride = 8u * blockDim.x;
+    constexpr uint32_t cstride = 8u * kBlock;   // (blockDim.x == kBlock): immediate offsets
     constexpr bool SCOLD = NPL > 1;
     const int CW = cold_words(S, SCOLD);   // words per node slot
     uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
@@ -136,13 +136,15 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     auto c_sl = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S) * cstride; };
     auto c_sl2 = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 1) * cstride; };
     auto c_ntr = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 2) * cstride; };
+    // the node's task count, stored only when its trace ends (for the summary)
+    auto c_cnt = [&](int jj) { return cbase + (uint32_t)(jj * CW + 2 * S + 3) * cstride; };
     // rarely used per-trace words (same column layout, after the node slots):
     // 0 trace index, 1 first task offset, 2 t_first, 3 error (task << 8 | field),
     // 4-6 the trace's cell (lambda1, lambda2, tau) with lmx_set_cell_params
     auto c_tw = [&](int k) { return cbase + (uint32_t)(NPL * CW + k) * cstride; };
     // SCOLD (several nodes per lane): a_[-1], mu, 1/(2 sigma^2), 1/(sigma sqrt(2 pi))
     // of each node also live in shared memory (read once per decision)
-    auto c_sc = [&](int jj, int f) { return cbase + (uint32_t)(jj * CW + 2 * S + 3 + f) * cstride; };
+    auto c_sc = [&](int jj, int f) { return cbase + (uint32_t)(jj * CW + 2 * S + 4 + f) * cstride; };
 
     // ---- per-trace (tile-replicated) state ----
     bool active = false, finished = false;
@@ -153,7 +155,8 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     int rate_lo = 0, rate_hi = 0;         // SeparateDynamic: inference arrivals in (now - W, now]
     int cur_defer = 0, status = LMX_OK;
     double r = kInf, t_last = -kInf, a_last_inf = -kInf, sum_ttft = 0.0;
-    long long n_slo = 0, sum_ver = 0, n_def = 0;
+    long long sum_ver = 0;
+    int n_slo = 0, n_def = 0;             // (<= 2^19 tasks, <= 2^20 decisions per trace)
     int n_mwait = 0, n_moff = 0;          // Algorithm 2 counters (MEM)
     int n_ck = 0;                         // Separate's checkpoints so far (sync model)
     double *ckt = (!LEMIX && p.sync_sep) ? p.ck + gtile * p.ck_cap : nullptr;
@@ -274,35 +277,27 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 sm.throughput = (sm.makespan > 0.0) ? (double)ntask / sm.makespan : 0.0;
                 sm.mean_ttft = (nI > 0) ? sum_ttft / (double)nI : 0.0;
                 sm.slo_attainment = (nI > 0) ? (double)n_slo / (double)nI : 1.0;
+                // node folds in node order by the tile's first lane, reading
+                // every lane's shared-memory column (no shuffles in this
+                // tile-divergent branch)
+#pragma unroll
+                for (int jj = 0; jj < NPL; ++jj) dev::sts_l(c_cnt(jj), cnt[jj]);
+                __syncwarp(tmask);
                 double U = 0.0, stds = 0.0;
                 long long act = 0;
-                for (int n = 0; n < N; ++n) {
-                    const int src = tbase + (n & (T - 1));
-                    const int jn = n >> log2T;
-                    long long c = 0, v2 = 0;
-#pragma unroll
-                    for (int jj = 0; jj < NPL; ++jj)
-                        if (jj == jn) {
-                            const long long a1 = dev::lds_l(c_sl(jj)), a2 = dev::lds_l(c_sl2(jj));
-                            c = cnt[jj];
-                            v2 = (long long)cnt[jj] * a2 - a1 * a1;
+                if (tl == 0) {
+                    for (int n = 0; n < N; ++n) {
+                        // lane tbase + (n mod T), slot n / T: its column is (n mod T) columns right
+                        const uint32_t col = 8u * (uint32_t)(n & (T - 1));
+                        const int jn = n >> log2T;
+                        const long long c = dev::lds_l(c_cnt(0) + (uint32_t)(jn * CW) * cstride + col);
+                        const long long a1 = dev::lds_l(c_sl(0) + (uint32_t)(jn * CW) * cstride + col);
+                        const long long a2 = dev::lds_l(c_sl2(0) + (uint32_t)(jn * CW) * cstride + col);
+                        for (int s = 0; s < S; ++s) U = U + dev::lds_d(c_busy(0, s) + (uint32_t)(jn * CW) * cstride + col);
+                        if (c > 0) {
+                            act++;
+                            stds = stds + sqrt((double)(c * a2 - a1 * a1)) / (double)c;
                         }
-#pragma unroll
-                    for (int s = 0; s < SMAX; ++s) {
-                        if (s < S) {
-                            double bv = 0.0;
-#pragma unroll
-                            for (int jj = 0; jj < NPL; ++jj)
-                                if (jj == jn) bv = dev::lds_d(c_busy(jj, s));
-                            U = U + dev::shfl_d(tmask, bv, src);
-                        }
-                    }
-                    double sd = (c > 0) ? sqrt((double)v2) / (double)c : 0.0;
-                    sd = dev::shfl_d(tmask, sd, src);
-                    c = __shfl_sync(tmask, c, src);
-                    if (c > 0) {
-                        act++;
-                        stds = stds + sd;
                     }
                 }
                 sm.active_nodes = act;

@@ -1,6 +1,9 @@
 """World-size-2 gloo test of the multi-GPU host logic (sharding, the one
 cross-rank summary reduction, max-over-ranks timing).  Runs on CPU; the
-per-shard schedules come from the oracle standing in for each GPU."""
+per-shard schedules come from the oracle standing in for each GPU.  The MC
+case shards with bench.shard_traces -- the exact call bench.py makes on every
+rank under torchrun (strong scaling: t = rank mod world of one fixed seed
+set)."""
 from __future__ import annotations
 
 import os
@@ -79,6 +82,57 @@ def test_world2_sharding_and_reduction():
     ref = ldist.cells_from_summaries(sums, _cells_of(TRACES), n_cells=6)
     for _, _, total, slowest in res:
         assert slowest == 2.0
+        for k in ldist.CELL_INT:
+            assert np.array_equal(total[k], ref[k]), k
+        for k in ldist.CELL_F64:
+            np.testing.assert_allclose(total[k], ref[k], rtol=1e-12, err_msg=k)
+
+
+MC_TOTAL, MC_INF, MC_TRAIN = 16, 400, 300
+
+
+def _mc_worker(rank, world, port, q):
+    import sys
+
+    import torch.distributed as dist
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        tr = bench.shard_traces(MC_TOTAL, rank, world, 3, MC_INF, MC_TRAIN, "strong")
+        assert tr.n_traces == bench.traces_on_rank(MC_TOTAL, rank, world, "strong")
+        ef, eb = workload.profile(N, S)
+        sums, _, _, _ = oracle.run_batch(ef, eb, N, S, tr, oracle.OracleParams(), outputs=False)
+        total = ldist.allreduce_cells(ldist.cells_from_summaries(sums))
+        q.put((rank, total, sums["n_slo_met"].tolist()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_mc_strong_shards_equal_the_single_run():
+    """The bench's strong-scaling shards of the fixed MC seed set, reduced
+    across two ranks, give the single-process totals of the whole set."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_mc_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=180) for _ in range(world)], key=lambda x: x[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    full = workload.mc_traces(MC_TOTAL, seed_base=3, n_inf=MC_INF, n_train=MC_TRAIN, with_out_len=False)
+    ef, eb = workload.profile(N, S)
+    sums, _, _, _ = oracle.run_batch(ef, eb, N, S, full, oracle.OracleParams(), outputs=False)
+    ref = ldist.cells_from_summaries(sums)
+    # per-trace results of each shard are the full run's rows t = rank mod 2
+    for rank, _, slo in res:
+        assert slo == sums["n_slo_met"][rank::world].tolist()
+    for _, total, _ in res:
         for k in ldist.CELL_INT:
             assert np.array_equal(total[k], ref[k]), k
         for k in ldist.CELL_F64:

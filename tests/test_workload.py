@@ -75,3 +75,17 @@ def test_mc_traces_half_bursty():
     g = [np.diff(tr.trace(t).arrival[:2000]) for t in range(8)]
     cv = [x.std() / x.mean() for x in g]
     assert max(cv[:4]) < 1.3 and min(cv[4:]) > 1.8
+
+
+def test_mc_subset_equals_the_full_set_rows():
+    """A rank's strided shard (bench.shard_traces, strong scaling) holds exactly
+    the rows the full fixed seed set has for those trace indices."""
+    full = workload.mc_traces(64, seed_base=7, n_inf=300, n_train=200, with_out_len=False)
+    for rank, world in ((0, 1), (1, 4), (3, 4), (5, 8)):
+        idx = np.arange(rank, 64, world)
+        sub = workload.mc_traces_subset(idx, 64, 7, 300, 200, with_out_len=False)
+        ref = full.subset(idx)
+        assert np.array_equal(sub.offsets, ref.offsets)
+        assert np.array_equal(sub.arrival.view(np.int64), ref.arrival.view(np.int64))
+        assert np.array_equal(sub.lbk, ref.lbk)
+        assert np.array_equal(sub.n_inf, ref.n_inf)

@@ -58,6 +58,9 @@ def _load():
         _lib.wl_generate.restype = ctypes.c_int
         _lib.wl_generate.argtypes = [ctypes.POINTER(_Spec), ctypes.c_int64, ctypes.c_uint64,
                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        _lib.wl_generate_seeds.restype = ctypes.c_int
+        _lib.wl_generate_seeds.argtypes = [ctypes.POINTER(_Spec), ctypes.c_int64, ctypes.c_void_p,
+                                           ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
     return _lib
 
 
@@ -258,6 +261,41 @@ def mc_traces(n_traces=65536, seed_base=1, n_inf=10000, n_train=10000, n_threads
     return Traces(offsets, np.full(n_traces, n_inf, np.int32), arrival, lbk, out_len)
 
 
-__all__ = ["WorkloadSpec", "Traces", "generate", "concat", "from_lists", "pack", "unpack", "profile",
+def mc_traces_subset(idx, n_total=65536, seed_base=1, n_inf=10000, n_train=10000, n_threads=None, out=None,
+                     with_out_len=True) -> Traces:
+    """Traces idx (sorted indices into the n_total-trace Monte Carlo set of
+    mc_traces(n_total, seed_base)): trace t is Poisson when t < n_total // 2,
+    bursty otherwise, with seed seed_base + t -- the same arrays mc_traces
+    would give for those indices (a rank's shard of the fixed seed set)."""
+    idx = np.asarray(idx, np.int64)
+    if idx.size and (np.any(np.diff(idx) <= 0) or idx[0] < 0 or idx[-1] >= n_total):
+        raise ValueError("idx must be sorted, unique and in [0, n_total)")
+    half = n_total // 2
+    per = n_inf + n_train
+    m = per * len(idx)
+    if out is None:
+        arrival = np.empty(m, np.float64)
+        lbk = np.empty(m, np.uint32)
+    else:
+        arrival, lbk = out
+    out_len = np.empty(m, np.uint32) if with_out_len else None
+    if n_threads is None:
+        n_threads = os.cpu_count() or 1
+    lib = _load()
+    k = int(np.searchsorted(idx, half))
+    for lo, hi, bursty in ((0, k, False), (k, len(idx), True)):
+        if hi <= lo:
+            continue
+        seeds = np.ascontiguousarray(seed_base + idx[lo:hi], np.uint64)
+        rc = lib.wl_generate_seeds(ctypes.byref(mc_spec(bursty, n_inf, n_train)._c()), hi - lo, seeds.ctypes.data,
+                                   arrival[lo * per:].ctypes.data, lbk[lo * per:].ctypes.data,
+                                   None if out_len is None else out_len[lo * per:].ctypes.data, n_threads)
+        if rc != 0:
+            raise ValueError("invalid workload spec")
+    offsets = np.arange(len(idx) + 1, dtype=np.int64) * per
+    return Traces(offsets, np.full(len(idx), n_inf, np.int32), arrival, lbk, out_len)
+
+
+__all__ = ["mc_traces_subset", "WorkloadSpec", "Traces", "generate", "concat", "from_lists", "pack", "unpack", "profile",
            "tiny_spec", "paper_spec", "sweep_spec", "large_spec", "mc_spec", "mc_traces", "SWEEP_RATES",
            "TABLE1", "replace"]

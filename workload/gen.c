@@ -141,6 +141,7 @@ static void gen_trace(const wl_spec *sp, uint64_t seed, double *arr, uint32_t *l
 typedef struct {
     const wl_spec *sp;
     uint64_t seed_base;
+    const uint64_t *seeds;   /* non-NULL: trace t uses seeds[t] */
     int64_t t0, t1;
     double *arr;
     uint32_t *lbk, *out_len;
@@ -151,15 +152,13 @@ static void *worker(void *p)
     job_t *j = (job_t *)p;
     int64_t per = j->sp->n_inf + j->sp->n_train;
     for (int64_t t = j->t0; t < j->t1; ++t)
-        gen_trace(j->sp, j->seed_base + (uint64_t)t, j->arr + t * per, j->lbk + t * per,
+        gen_trace(j->sp, j->seeds ? j->seeds[t] : j->seed_base + (uint64_t)t, j->arr + t * per, j->lbk + t * per,
                   j->out_len ? j->out_len + t * per : NULL);
     return NULL;
 }
 
-/* Fill n_traces fixed-size traces (n_inf + n_train tasks each, contiguous).
- * Trace t uses seed seed_base + t.  Returns 0 on success. */
-int wl_generate(const wl_spec *sp, int64_t n_traces, uint64_t seed_base,
-                double *arrival, uint32_t *lbk, uint32_t *out_len, int n_threads)
+static int generate(const wl_spec *sp, int64_t n_traces, uint64_t seed_base, const uint64_t *seeds,
+                    double *arrival, uint32_t *lbk, uint32_t *out_len, int n_threads)
 {
     if (!sp || n_traces < 0 || sp->n_inf < 0 || sp->n_train < 0) return 1;
     if (sp->n_inf > 0 && !(sp->rate_inf > 0.0)) return 1;
@@ -173,7 +172,7 @@ int wl_generate(const wl_spec *sp, int64_t n_traces, uint64_t seed_base,
     pthread_t th[256];
     job_t jobs[256];
     for (int k = 0; k < n_threads; ++k) {
-        jobs[k].sp = sp; jobs[k].seed_base = seed_base;
+        jobs[k].sp = sp; jobs[k].seed_base = seed_base; jobs[k].seeds = seeds;
         jobs[k].t0 = n_traces * k / n_threads; jobs[k].t1 = n_traces * (k + 1) / n_threads;
         jobs[k].arr = arrival; jobs[k].lbk = lbk; jobs[k].out_len = out_len;
     }
@@ -181,4 +180,21 @@ int wl_generate(const wl_spec *sp, int64_t n_traces, uint64_t seed_base,
     for (int k = 0; k < n_threads; ++k) pthread_create(&th[k], NULL, worker, &jobs[k]);
     for (int k = 0; k < n_threads; ++k) pthread_join(th[k], NULL);
     return 0;
+}
+
+/* Fill n_traces fixed-size traces (n_inf + n_train tasks each, contiguous).
+ * Trace t uses seed seed_base + t.  Returns 0 on success. */
+int wl_generate(const wl_spec *sp, int64_t n_traces, uint64_t seed_base,
+                double *arrival, uint32_t *lbk, uint32_t *out_len, int n_threads)
+{
+    return generate(sp, n_traces, seed_base, NULL, arrival, lbk, out_len, n_threads);
+}
+
+/* The same for an explicit seed list: trace t uses seeds[t] (a rank's shard
+ * of a fixed seed set).  Returns 0 on success. */
+int wl_generate_seeds(const wl_spec *sp, int64_t n_traces, const uint64_t *seeds,
+                      double *arrival, uint32_t *lbk, uint32_t *out_len, int n_threads)
+{
+    if (!seeds && n_traces > 0) return 1;
+    return generate(sp, n_traces, 0, seeds, arrival, lbk, out_len, n_threads);
 }
