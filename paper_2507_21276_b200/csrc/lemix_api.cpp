@@ -572,31 +572,15 @@ lmx_status lmx_run(lmx_ctx *c)
     k.fixed = c->has_fixed ? (const int32_t *)c->fixed.p : nullptr;
     k.eta = (const double *)c->eta.p;
 
-    // kernel: the lane-per-trace loop for small clusters (one trace per
-    // thread, candidates unrolled), the tile-of-lanes loop otherwise;
-    // LMX_KERNEL=tile|lane overrides (developer A/B; lane must be supported)
-    bool lane = lmx::lane_supported(k);
-    if (const char *force = getenv("LMX_KERNEL")) {
-        if (!strcmp(force, "tile")) lane = false;
-        else if (!strcmp(force, "lane") && !lane)
-            return c->fail(LMX_EINVAL, "LMX_KERNEL=lane: needs N <= 4, S <= 2, no memory model, no cell params");
-    }
-    if (lane) {
-        k.T = 1;
-        k.log2T = 0;
-        k.npl = c->N;
-        k.npad = lmx::lane_nodes_bucket(c->N);
-    }
-
     // geometry: persistent grid = resident CTAs, capped by the number of traces
     int occ_err = 0;
-    const int per_sm = lane ? lmx::lane_occupancy(k, &occ_err) : lmx::event_loop_occupancy(k, &occ_err);
+    const int per_sm = lmx::event_loop_occupancy(k, &occ_err);
     if (occ_err != 0 || per_sm < 1)
         return c->fail(LMX_ECUDA, std::string("event loop occupancy query failed: ") +
                                       cudaGetErrorString((cudaError_t)occ_err));
     int n_sm = 0;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
-    const int block = lane ? lmx::lane_block_threads() : lmx::event_loop_block_threads();
+    const int block = lmx::event_loop_block_threads();
     const int tiles_per_block = block / k.T;
     int64_t grid = (int64_t)n_sm * per_sm;
     const int64_t need = (T + tiles_per_block - 1) / tiles_per_block;
@@ -710,7 +694,7 @@ lmx_status lmx_run(lmx_ctx *c)
     c->launches = 0;
     cudaEventRecord(c->ev0, c->stream);
     if (T > 0) {
-        int e = lane ? lmx::launch_lane_loop(k, (int)grid, c->stream) : lmx::launch_event_loop(k, (int)grid, c->stream);
+        int e = lmx::launch_event_loop(k, (int)grid, c->stream);
         if (e != 0) {
             if (stream_in) cudaStreamSynchronize(c->copy_stream);
             return c->cuda((cudaError_t)e, "event loop launch");
@@ -740,7 +724,7 @@ lmx_status lmx_run(lmx_ctx *c)
     c->grid = (int32_t)grid;
     c->block = block;
     c->lanes = k.T;
-    c->smem = lane ? lmx::lane_smem_bytes(k) : lmx::event_loop_smem_bytes(k);
+    c->smem = lmx::event_loop_smem_bytes(k);
     c->ran = true;
     c->synced = false;
     return LMX_OK;

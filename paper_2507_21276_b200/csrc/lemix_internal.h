@@ -95,13 +95,4 @@ int event_loop_occupancy(const KParams &p, int *err);
 int launch_event_loop(const KParams &p, int grid, void *stream);
 int launch_cells(const CellParams &c, void *stream);
 
-// lane-per-trace event loop (lemix_lane.cu): N <= 4, S <= 2, no Algorithm 2
-// memory model, no per-cell parameters
-bool lane_supported(const KParams &p);
-int lane_nodes_bucket(int N);
-int lane_block_threads();
-int lane_smem_bytes(const KParams &p);
-int lane_occupancy(const KParams &p, int *err);
-int launch_lane_loop(const KParams &p, int grid, void *stream);
-
 }  // namespace lmx

@@ -19,18 +19,6 @@ def P(**kw):
     return lemix.Params(**kw)
 
 
-@pytest.fixture(autouse=True, params=["default", "tile"])
-def kernel_variant(request, monkeypatch):
-    """Every parity case runs on the kernel lmx_run picks (the lane-per-trace
-    loop for N <= 4, S <= 2; the tile loop otherwise) and again forced onto
-    the tile-of-lanes loop, so both event loops stay bit-exact."""
-    if request.param == "tile":
-        monkeypatch.setenv("LMX_KERNEL", "tile")
-    else:
-        monkeypatch.delenv("LMX_KERNEL", raising=False)
-    return request.param
-
-
 POLICIES = [lemix.LMX_LEMIX, lemix.LMX_RR, lemix.LMX_SEPARATE]
 
 
