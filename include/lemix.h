@@ -60,18 +60,25 @@ typedef enum {
     LMX_EBUDGET = 7   /* per trace: decision budget exhausted (cannot happen for valid input) */
 } lmx_status;
 
-typedef enum { LMX_LEMIX = 0, LMX_RR = 1, LMX_SEPARATE = 2, LMX_FIXED = 3 } lmx_policy;
+/* LMX_MIXLUF: the Mix-LUF comparison system (DESIGN.md
+ * R-luf): the node with the least busy time committed so far (lowest
+ * average utilisation; ties -> lowest index), each decision dispatched after
+ * a serialised utilisation query of params.luf_delay seconds. */
+typedef enum { LMX_LEMIX = 0, LMX_RR = 1, LMX_SEPARATE = 2, LMX_FIXED = 3, LMX_MIXLUF = 4 } lmx_policy;
 typedef enum { LMX_HOST = 0, LMX_DEVICE = 1 } lmx_mem;
 
 /* Profile table (offline profiling, §4.1): stage latencies
  * Δ_F = eta_f·C·ℓ², Δ_B = eta_b·C·ℓ².  Host memory, node-major
  * [n_nodes * n_stages], every value finite and > 0.  1 <= n_nodes <= 128,
- * 1 <= n_stages <= 16.  Copied. */
+ * 1 <= n_stages <= 16.  eta_d (may be NULL = 0): seconds per context token
+ * per item of one decode step on that GPU (continuous batching
+ * only), finite and >= 0.  Copied. */
 typedef struct {
     int32_t n_nodes;
     int32_t n_stages;
     const double *eta_f;
     const double *eta_b;
+    const double *eta_d;
 } lmx_profile;
 
 /* Task packing of len_batch_kind: query length ℓ in bits 0-11 (1..2048),
@@ -99,6 +106,11 @@ typedef struct {
     const double *arrival;
     const uint32_t *len_batch_kind;
     const int32_t *fixed_node;
+    /* out_len[n_tasks]: decode steps of an inference request (tokens after
+     * the prefill's first, 0..2048).  Read only with continuous
+     * batching (params.cb_cmax > 0), else may be NULL.  Same memory kind as
+     * arrival. */
+    const uint32_t *out_len;
 } lmx_traces;
 
 /* Scheduler parameters.  lmx_params_default() fills the DESIGN.md defaults:
@@ -161,6 +173,21 @@ typedef struct {
      * value -> LMX_EINVAL. */
     int32_t debug_level;
     int32_t debug_pad;     /* zero */
+    /* Algorithm 3 ContinuousBatching with hybrid prefill/decode (PAPER.md:
+     * 689-727; DESIGN.md R-cb).  cb_cmax = 0 (default):
+     * every request is placed on its own.  cb_cmax = C >= 1: inference
+     * requests are grouped FCFS into batches of up to C (a batch waits at
+     * most cb_tw seconds after its first request and stops at a released
+     * training task); a batch is placed as one task (C = its members' total,
+     * l = the longest, padded) whose decode steps then run on the same node
+     * (eta_d); per request TTFT and TBT are reported.  Not
+     * combined with mem_enable (-> LMX_EINVAL). */
+    int32_t cb_cmax;
+    /* Eq. 4 reading: 0 = R-14 (the node's latest forward end), 1 = R-14b
+     * (also counting the training task's own forward).  DESIGN.md. */
+    int32_t eq4_mode;
+    double cb_tw;          /* T_w seconds, finite and >= 0 */
+    double luf_delay;      /* LMX_MIXLUF: scheduler latency per decision, seconds (>= 0) */
 } lmx_params;
 
 /* Per-trace summary (metrics of PAPER.md:786-790).  For a trace whose status
@@ -174,12 +201,16 @@ typedef struct {
     int64_t status;         /* lmx_status of this trace */
     int64_t n_mem_wait;     /* Algorithm 2: stage forwards that waited for memory */
     int64_t n_offload;      /* Algorithm 2: stage forwards whose activations were offloaded */
+    int64_t n_batches;      /* Algorithm 3: inference batches placed (cb_cmax > 0), else 0 */
+    int64_t n_tbt;          /* Algorithm 3: requests with >= 1 decode step (TBT defined) */
     double makespan;        /* last completion - first arrival */
     double throughput;      /* tasks / makespan */
     double sum_ttft, mean_ttft;
     double slo_attainment;  /* n_slo_met / n_inf (1.0 when n_inf == 0) */
     double mean_util;       /* Σ busy / (N·S·makespan) */
     double mean_len_std;    /* mean over active nodes of the population σ of lengths */
+    double sum_tbt, mean_tbt;   /* time-between-tokens: per request, the mean gap
+                                   between its tokens; summed / averaged over requests */
 } lmx_summary;
 
 /* Aggregate of the per-trace summaries of one cell (e.g. one (rate, policy)

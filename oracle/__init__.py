@@ -18,13 +18,13 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liblemix_oracle.so")
 
-LEMIX, RR, SEPARATE, FIXED = 0, 1, 2, 3
+LEMIX, RR, SEPARATE, FIXED, MIXLUF = 0, 1, 2, 3, 4
 OK, EINVAL, EQCAP, EBUDGET = 0, 1, 6, 7
 
 
 class Profile(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int32), ("n_stages", ctypes.c_int32),
-                ("eta_f", ctypes.c_void_p), ("eta_b", ctypes.c_void_p)]
+                ("eta_f", ctypes.c_void_p), ("eta_b", ctypes.c_void_p), ("eta_d", ctypes.c_void_p)]
 
 
 class Params(ctypes.Structure):
@@ -37,13 +37,14 @@ class Params(ctypes.Structure):
                 ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double),
                 ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double),
                 ("sep_dynamic", ctypes.c_int32), ("sep_pad", ctypes.c_int32), ("dyn_rate", ctypes.c_double),
-                ("dyn_window", ctypes.c_double)]
+                ("dyn_window", ctypes.c_double), ("cb_cmax", ctypes.c_int32), ("eq4_mode", ctypes.c_int32),
+                ("cb_tw", ctypes.c_double), ("luf_delay", ctypes.c_double)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes",
-               "sum_version", "status", "n_mem_wait", "n_offload")
+               "sum_version", "status", "n_mem_wait", "n_offload", "n_batches", "n_tbt")
 SUMMARY_F64 = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util",
-               "mean_len_std")
+               "mean_len_std", "sum_tbt", "mean_tbt")
 
 
 class Summary(ctypes.Structure):
@@ -77,11 +78,11 @@ def _load(textbook: bool = False):
         vp = ctypes.c_void_p
         lib.orc_run_trace.restype = ctypes.c_int
         lib.orc_run_trace.argtypes = [ctypes.POINTER(Profile), ctypes.POINTER(Params), ctypes.c_int64,
-                                      ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                       ctypes.POINTER(Summary), ctypes.POINTER(Counters)]
         lib.orc_run_batch.restype = ctypes.c_int
         lib.orc_run_batch.argtypes = [ctypes.POINTER(Profile), ctypes.POINTER(Params), ctypes.c_int64,
-                                      vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(Counters)]
+                                      vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, ctypes.POINTER(Counters)]
         lib.orc_exp_neg.restype = ctypes.c_double
         lib.orc_exp_neg.argtypes = [ctypes.c_double]
         _libs[path] = lib
@@ -115,13 +116,20 @@ class OracleParams:
     sep_dynamic: int = 0
     dyn_rate: float = 50.0
     dyn_window: float = 10.0
+    # Algorithm 3 continuous batching (NEXT-2, DESIGN.md R-cb); 0 = off
+    cb_cmax: int = 0
+    cb_tw: float = 0.0
+    # Eq. 4 reading (R-14 / R-14b)
+    eq4_mode: int = 0
+    # Mix-LUF scheduler latency per decision (DESIGN.md R-luf)
+    luf_delay: float = 0.0
 
     def _c(self) -> Params:
         return Params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1,
                       self.lambda2, self.tau, self.slo_mult, self.slo_const, self.sigma_floor,
                       self.lc0, self.alpha, self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax,
                       self.mem_pen, self.sync_interval, 0, self.sync_latency, self.sep_dynamic, 0, self.dyn_rate,
-                      self.dyn_window)
+                      self.dyn_window, self.cb_cmax, self.eq4_mode, self.cb_tw, self.luf_delay)
 
 
 def _ptr(a):
@@ -132,28 +140,36 @@ def exp_neg(t: float, textbook: bool = False) -> float:
     return _load(textbook).orc_exp_neg(float(t))
 
 
+def _eta_d(eta_d):
+    return None if eta_d is None else np.ascontiguousarray(eta_d, np.float64)
+
+
 def run_trace(eta_f, eta_b, n_nodes, n_stages, arrival, lbk, n_inf, params: OracleParams,
-              fixed_node=None, want_paths=False, want_cand=False):
-    """Run one trace; returns a dict of per-task outputs, summary, counters."""
+              fixed_node=None, want_paths=False, want_cand=False, out_len=None, eta_d=None):
+    """Run one trace; returns a dict of per-task outputs, summary, counters.
+    out_len / eta_d: output tokens per task and decode cost table (continuous
+    batching only)."""
     lib = _load()
     eta_f = np.ascontiguousarray(eta_f, np.float64)
     eta_b = np.ascontiguousarray(eta_b, np.float64)
+    eta_d = _eta_d(eta_d)
     arrival = np.ascontiguousarray(arrival, np.float64)
     lbk = np.ascontiguousarray(lbk, np.uint32)
+    out_len = None if out_len is None else np.ascontiguousarray(out_len, np.uint32)
     m = len(arrival)
-    prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data)
+    prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data, _ptr(eta_d))
     par = params._c()
     node_defer = np.zeros(m, np.uint32)
     dec = np.full(m, -1, np.int32)
     comp = np.zeros(m, np.float64)
     sf1 = np.zeros(m, np.float64)
     paths = np.zeros(m * n_stages * 4, np.float64) if want_paths else None
-    cand = np.zeros(max(m, 1) * n_nodes * 3, np.float64) if want_cand else None
+    cand = np.full(max(m, 1) * n_nodes * 3, np.nan) if want_cand else None
     fixed = None if fixed_node is None else np.ascontiguousarray(fixed_node, np.int32)
     sm = Summary()
     ct = Counters()
     st = lib.orc_run_trace(ctypes.byref(prof), ctypes.byref(par), m, int(n_inf), arrival.ctypes.data,
-                           lbk.ctypes.data, _ptr(fixed), node_defer.ctypes.data, dec.ctypes.data,
+                           lbk.ctypes.data, _ptr(out_len), _ptr(fixed), node_defer.ctypes.data, dec.ctypes.data,
                            comp.ctypes.data, sf1.ctypes.data, _ptr(paths), _ptr(cand), ctypes.byref(sm),
                            ctypes.byref(ct))
     out = dict(status=st, node=(node_defer & 0xFFFF).astype(np.int32), defer=(node_defer >> 16).astype(np.int32),
@@ -168,13 +184,17 @@ def run_trace(eta_f, eta_b, n_nodes, n_stages, arrival, lbk, n_inf, params: Orac
 
 
 def run_batch(eta_f, eta_b, n_nodes, n_stages, traces, params: OracleParams, fixed_node=None,
-              outputs=True, textbook=False):
-    """Run a CSR batch (workload.Traces).  Returns (summaries structured array,
-    per-task dict or None, counters dict, first error status)."""
+              outputs=True, textbook=False, eta_d=None):
+    """Run a CSR batch (workload.Traces; its out_len is passed when continuous
+    batching is on).  Returns (summaries structured array, per-task dict or
+    None, counters dict, first error status)."""
     lib = _load(textbook)
     eta_f = np.ascontiguousarray(eta_f, np.float64)
     eta_b = np.ascontiguousarray(eta_b, np.float64)
-    prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data)
+    eta_d = _eta_d(eta_d)
+    prof = Profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data, _ptr(eta_d))
+    out_len = (np.ascontiguousarray(traces.out_len, np.uint32)
+               if params.cb_cmax > 0 and traces.out_len is not None else None)
     par = params._c()
     m = traces.n_tasks
     T = traces.n_traces
@@ -190,7 +210,7 @@ def run_batch(eta_f, eta_b, n_nodes, n_stages, traces, params: OracleParams, fix
     arrival = np.ascontiguousarray(traces.arrival, np.float64)
     lbk = np.ascontiguousarray(traces.lbk, np.uint32)
     st = lib.orc_run_batch(ctypes.byref(prof), ctypes.byref(par), T, offsets.ctypes.data,
-                           n_inf.ctypes.data, arrival.ctypes.data, lbk.ctypes.data, _ptr(fixed),
+                           n_inf.ctypes.data, arrival.ctypes.data, lbk.ctypes.data, _ptr(out_len), _ptr(fixed),
                            _ptr(node_defer), _ptr(dec), _ptr(comp), _ptr(sf1), sums.ctypes.data,
                            ctypes.byref(ct))
     per_task = None

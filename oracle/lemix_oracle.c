@@ -17,6 +17,9 @@
  *   - baselines Separate / NaiveMix(RR)                                PAPER.md:795-796 (§6.1)
  *   - metrics (throughput, SLO = TTFT <= 5x forward latency)          PAPER.md:786-790 (§6.1)
  *   - ExecuteTaskMemoryAware   Algorithm 2, lines 1-20 (optional)      PAPER.md:608-641 (§4.4)
+ *   - ContinuousBatching       Algorithm 3, lines 1-17 (optional), with
+ *                              hybrid prefill/decode and TBT           PAPER.md:689-727, 789 (§5.4, §6.1)
+ *   - Mix-LUF baseline         lowest average utilisation first        PAPER.md:797, 1101 (§6.1, Table 2)
  *
  * Where the paper is silent or garbled the DESIGN.md reading is cited as
  * [R-n] (DESIGN.md §"Readings").  Floating point: IEEE binary64, built with
@@ -89,6 +92,8 @@ double orc_exp_neg(double t)
  * ------------------------------------------------------------------------- */
 typedef struct {
     double sf[MAXS], ef[MAXS];   /* forward path  start_f^s, end_f^s */
+    double oe[MAXS];             /* occupancy end of GPU (n, s): end_f^s + the decode steps that
+                                    follow the prefill there ([R-cb]); = end_f^s without batching */
     double sb[MAXS], eb[MAXS];   /* backward path start_b^s, end_b^s (training only) */
     int off[MAXS];               /* Algorithm 2: activations offloaded from GPU s (line 10) */
 } path_t;
@@ -111,6 +116,7 @@ typedef struct {
     int N, S;
     const double *arrival;
     const uint32_t *lbk;
+    const uint32_t *out_len;
     path_t *path;           /* per task */
     node_t *node;
     orc_counters *cnt;
@@ -129,19 +135,27 @@ static double task_w(uint32_t v)
 
 static double eta_f(const trace_t *T, int n, int s) { return T->prof->eta_f[n * T->S + s]; }
 static double eta_b(const trace_t *T, int n, int s) { return T->prof->eta_b[n * T->S + s]; }
+static double eta_d(const trace_t *T, int n, int s) { return T->prof->eta_d ? T->prof->eta_d[n * T->S + s] : 0.0; }
 
 /* ---------------------------------------------------------------------------
  * Algorithm 1  ComputeIdleness.  Line numbers below are
  * the algorithm's own.  Returns II and R; writes the planned forward path of
- * the new task into sf/ef.  Entries of Q_train^n for which CheckExecuted holds
- * (lines 17-18) are removed from the node's queue on return.
+ * the new task into sf/ef (and its occupancy ends into oe).  Entries of
+ * Q_train^n for which CheckExecuted holds (lines 17-18) are removed from the
+ * node's queue on return.
+ *
+ * w = C*l^2 of the task.  tail[s] (NULL = none) is the decode work a
+ * continuous batch runs on GPU s right after its prefill ([R-cb]): the GPU is
+ * busy until end + tail[s], so that occupancy end is what must fit before a
+ * pending backward (line 10) and what the next task on the node starts after
+ * (line 3's task_prev); the next stage still starts at the prefill end (the
+ * first token flows on).  With no tail every occ equals end bit for bit.
  * ------------------------------------------------------------------------- */
-static void compute_idleness(trace_t *T, int n, uint32_t task_lbk, double a, double now,
-                             double *II_out, double *R_out, double *sf, double *ef)
+static void compute_idleness(trace_t *T, int n, double w, const double *tail, double a, double now,
+                             double *II_out, double *R_out, double *sf, double *ef, double *oe)
 {
     const int S = T->S;
     node_t *nd = &T->node[n];
-    const double w = task_w(task_lbk);
     T->cnt->alg1_calls++;
 
     /* line 3: task_prev <- Q^n[-1].  A node that never ran a task has a
@@ -149,7 +163,7 @@ static void compute_idleness(trace_t *T, int n, uint32_t task_lbk, double a, dou
      * start it ([R-1]); its a_[-1] is a itself ([R-9]). */
     double prev_ef[MAXS];
     if (nd->last_task >= 0) {
-        for (int s = 0; s < S; ++s) prev_ef[s] = T->path[nd->last_task].ef[s];
+        for (int s = 0; s < S; ++s) prev_ef[s] = T->path[nd->last_task].oe[s];
     } else {
         double v = a;
         for (int s = 0; s < S; ++s) { prev_ef[s] = v; v = v + eta_f(T, n, s) * w; }
@@ -167,14 +181,16 @@ static void compute_idleness(trace_t *T, int n, uint32_t task_lbk, double a, dou
     for (int s = 0; s < S; ++s) {                      /* line 4 */
         T->cnt->stage_iters++;
         const double dF = eta_f(T, n, s) * w;
+        const double dD = tail ? tail[s] : 0.0;
         double start = MAX(end_prev_stage, prev_ef[s]);  /* line 5 */
         double end = start + dF;                          /* line 6 */
+        double occ = end + dD;
         double offset = 0.0;                              /* line 7 */
         while (front < qlen) {                            /* line 8 */
             int64_t k = front;
             int64_t tt = qtemp[front++];                  /* line 9: dequeue */
             const path_t *pt = &T->path[tt];
-            if (end <= pt->sb[s]) {                       /* line 10 */
+            if (occ <= pt->sb[s]) {                       /* line 10 */
                 front--;                                  /* line 11: reinstated at the front ([R-3]) */
                 T->cnt->scan_break++;
                 break;                                    /* line 12 */
@@ -182,6 +198,7 @@ static void compute_idleness(trace_t *T, int n, uint32_t task_lbk, double a, dou
             T->cnt->scan_consumed++;
             start = MAX(start, pt->eb[s]);                /* line 13 */
             end = start + dF;                             /* line 14 */
+            occ = end + dD;
             if (prev_ef[s] <= pt->sb[s]) {                /* line 15 */
                 offset = offset + eta_b(T, n, s) * task_w(T->lbk[tt]);   /* line 16 ([R-7]) */
                 T->cnt->offset_adds++;
@@ -195,6 +212,7 @@ static void compute_idleness(trace_t *T, int n, uint32_t task_lbk, double a, dou
         II = II + ((start - prev_ef[s]) - offset);        /* line 19 ([R-8], grouping [R-II]) */
         sf[s] = start;
         ef[s] = end;
+        oe[s] = occ;
         end_prev_stage = end;
     }
     *II_out = II;
@@ -271,8 +289,12 @@ static double tau_R(const trace_t *T, uint32_t v)
 
 /* Eq. 4: defer the training task iff
  *   min_n { max_{task in Q^n} end_f^S + η_F^n·C'ℓ'² } - a' > tau_R
- * for the next enqueued inference task (a', ℓ', C') ([R-14], [R-15]). */
-static int should_deprioritize(trace_t *T, uint32_t next_lbk, double a_next)
+ * for the next enqueued inference task (a', ℓ', C') ([R-14], [R-15]).
+ * eq4_mode 1 ([R-14b]): the inner term also counts the training task's own
+ * forward, as if it went to node n ahead of the inference task: its forward
+ * chained stage by stage after the node's last forward ends (no backward
+ * scan), x_n = that end + η_F^{n,S}·C'ℓ'². */
+static int should_deprioritize(trace_t *T, uint32_t next_lbk, double a_next, double a_train, double w_train)
 {
     const int N = T->N, S = T->S;
     T->cnt->eq4_checks++;
@@ -280,11 +302,70 @@ static int should_deprioritize(trace_t *T, uint32_t next_lbk, double a_next)
     double m = INFINITY;
     for (int n = 0; n < N; ++n) {
         const node_t *nd = &T->node[n];
-        double latest = nd->has_efS ? nd->max_efS : -INFINITY;   /* max over empty Q^n */
+        double latest;
+        if (T->par->eq4_mode == 1) {
+            double v = a_train;
+            for (int s = 0; s < S; ++s) {
+                double pe = (nd->last_task >= 0) ? T->path[nd->last_task].oe[s] : -INFINITY;
+                v = MAX(v, pe) + eta_f(T, n, s) * w_train;
+            }
+            latest = v;
+        } else {
+            latest = nd->has_efS ? nd->max_efS : -INFINITY;   /* max over empty Q^n */
+        }
         double x = latest + eta_f(T, n, S - 1) * w;
         m = MIN(m, x);
     }
     return (m - a_next) > tau_R(T, next_lbk);
+}
+
+/* ---------------------------------------------------------------------------
+ * Algorithm 3  ContinuousBatching, lines 2-15, on the
+ * FCFS inference stream ([R-cb]).  The batch opens at the arrival of request
+ * i (line 5: T_start).  The next request joins (line 10) while the batch has
+ * fewer than C members (line 7), it is not preceded by a released training
+ * task (line 9: a training task at the head of the queue -- released at
+ * r_train before the request arrives; ties go to inference, [R-19]) and the
+ * timer has not run out (line 9: T_start + T_w > the request's arrival).  The
+ * batch executes (line 15) as soon as it is full -- at its C-th member's
+ * arrival -- else when the timer expires or the training task is released,
+ * whichever is first.  Returns the member count; *t_exec = that time.
+ * ------------------------------------------------------------------------- */
+static int64_t continuous_batch(const double *arrival, int64_t i, int64_t nI, int64_t C, double Tw,
+                                int train_pending, double r_train, double *t_exec)
+{
+    const double T_start = arrival[i];                    /* line 5 */
+    int64_t m = 1;                                        /* line 10: request i */
+    while (i + m < nI && m < C) {                         /* line 7 */
+        const double ar = arrival[i + m];                 /* line 8: get_next_request */
+        if (train_pending && r_train < ar) break;         /* line 9: require_backward -> line 12 */
+        if (!(T_start + Tw > ar)) break;                  /* line 9: timer -> line 12 */
+        m++;                                              /* line 10 */
+    }
+    if (m == C) *t_exec = arrival[i + m - 1];             /* full */
+    else *t_exec = MIN(T_start + Tw, train_pending ? r_train : INFINITY);
+    return m;
+}
+
+/* Decode work ([R-cb]): after the prefill, the batch
+ * decodes with hybrid iteration-level batching: step k = 1, 2,
+ * ... advances every member that still needs a token (C_k = members with
+ * out >= k; out = decode steps of a request, 0 = none) over a context padded
+ * to the batch's prompt length, l_pad + k - 1 tokens, at
+ * eta_D * C_k * (l_pad + k - 1) seconds on each GPU ("step latency = max over
+ * members of eta_D * C_batch * l_ctx").  Returns the work of
+ * steps 1 .. upto in exact integer token units, summed step by step; the
+ * seconds are eta_D times it (one rounding, like Delta_F = eta_F * C l^2). */
+static int64_t decode_work(const uint32_t *out, int64_t m, int64_t l_pad, int64_t upto)
+{
+    int64_t W = 0;
+    for (int64_t k = 1; k <= upto; ++k) {
+        int64_t Ck = 0;
+        for (int64_t jj = 0; jj < m; ++jj)
+            if ((int64_t)out[jj] >= k) Ck++;               /* members still decoding at step k */
+        W += Ck * (l_pad + k - 1);
+    }
+    return W;
 }
 
 /* Backward planning: immediately after the forward path,
@@ -354,7 +435,7 @@ static int execute_memory_aware(trace_t *T, int n, uint32_t v, double a, double 
     const int64_t tok = (int64_t)task_batch(v) * task_len(v);
     double prev_ef[MAXS];
     if (nd->last_task >= 0) {
-        for (int s = 0; s < S; ++s) prev_ef[s] = T->path[nd->last_task].ef[s];
+        for (int s = 0; s < S; ++s) prev_ef[s] = T->path[nd->last_task].oe[s];
     } else {
         double x = a;
         for (int s = 0; s < S; ++s) { prev_ef[s] = x; x = x + eta_f(T, n, s) * w; }
@@ -408,7 +489,7 @@ static int execute_memory_aware(trace_t *T, int n, uint32_t v, double a, double 
 
 int orc_run_trace(const orc_profile *prof, const orc_params *par,
                   int64_t n_tasks, int64_t n_inf,
-                  const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
+                  const double *arrival, const uint32_t *lbk, const uint32_t *out_len, const int32_t *fixed_node,
                   uint32_t *node_defer, int32_t *decision_idx, double *completion,
                   double *start_f1, double *paths, double *cand,
                   orc_summary *summary, orc_counters *counters)
@@ -422,10 +503,16 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 
     const int64_t nI = n_inf, nT = n_tasks - n_inf;
     sm.n_tasks = n_tasks; sm.n_inf = nI; sm.n_train = nT;
+    const int cb = par->cb_cmax > 0;   /* continuous batching (Algorithm 3) */
 
     /* ---- input validation (inputs must be finite, ordered and in range) ---- */
     int bad = (N < 1 || S < 1 || S > MAXS || nI < 0 || nT < 0 || par->qcap < 1 || !(par->lambda1 > 0.0));
+    bad = bad || par->policy < ORC_LEMIX || par->policy > ORC_MIXLUF;
     bad = bad || par->sync_interval < 0 || !(par->sync_latency >= 0.0 && par->sync_latency < INFINITY);
+    bad = bad || par->cb_cmax < 0 || (par->eq4_mode != 0 && par->eq4_mode != 1);
+    bad = bad || !(par->luf_delay >= 0.0 && par->luf_delay < INFINITY);
+    if (cb)   /* T_w finite, decode costs and output lengths given; not combined with Algorithm 2 */
+        bad = bad || !(par->cb_tw >= 0.0 && par->cb_tw < INFINITY) || par->mem_enable || (nI > 0 && !out_len);
     if (par->sep_dynamic)
         bad = bad || !(par->dyn_rate >= 0.0 && par->dyn_rate < INFINITY) ||
               !(par->dyn_window > 0.0 && par->dyn_window < INFINITY);
@@ -433,12 +520,14 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
         bad = bad || par->mem_cap < 0 || !(par->mem_dt > 0.0) || !(par->mem_tmax > 0.0 && par->mem_tmax < INFINITY) ||
               !(par->mem_pen >= 0.0 && par->mem_pen < INFINITY) || par->mem_tmax / par->mem_dt > 1048576.0;
     for (int k = 0; k < N * S && !bad; ++k)
-        bad = !(prof->eta_f[k] > 0.0 && prof->eta_f[k] < INFINITY && prof->eta_b[k] > 0.0 && prof->eta_b[k] < INFINITY);
+        bad = !(prof->eta_f[k] > 0.0 && prof->eta_f[k] < INFINITY && prof->eta_b[k] > 0.0 && prof->eta_b[k] < INFINITY) ||
+              (cb && prof->eta_d && !(prof->eta_d[k] >= 0.0 && prof->eta_d[k] < INFINITY));
     for (int64_t t = 0; t < n_tasks && !bad; ++t) {
         uint32_t v = lbk[t];
         bad = (v >> 21) != 0 || task_len(v) < 1 || task_len(v) > 2048 || task_batch(v) < 1 ||
               task_kind(v) != (t >= nI) || !(arrival[t] >= 0.0 && arrival[t] < INFINITY) ||
               (t > 0 && t < nI && arrival[t] < arrival[t - 1]) ||
+              (cb && t < nI && out_len[t] > 2048u) ||
               (par->policy == ORC_FIXED && (fixed_node[t] < 0 || fixed_node[t] >= N));
     }
     if (!bad && par->policy == ORC_SEPARATE && N == 1 && nI > 0 && nT > 0) bad = 1;
@@ -450,7 +539,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 
     trace_t T;
     T.prof = prof; T.par = par; T.N = N; T.S = S;
-    T.arrival = arrival; T.lbk = lbk; T.cnt = counters;
+    T.arrival = arrival; T.lbk = lbk; T.out_len = out_len; T.cnt = counters;
     T.path = (path_t *)calloc((size_t)(n_tasks > 0 ? n_tasks : 1), sizeof(path_t));
     T.node = (node_t *)calloc((size_t)N, sizeof(node_t));
     for (int n = 0; n < N; ++n) {
@@ -480,27 +569,32 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
     int64_t rate_lo = 0, rate_hi = 0;   /* SeparateDynamic: arrivals in (now - W, now] */
     double r = (nT > 0) ? arrival[nI] : INFINITY;
     double t_last = -INFINITY;
+    double sched_free = -INFINITY;      /* Mix-LUF: when the scheduler finishes its previous query ([R-luf]) */
     int status = ORC_OK;
     double IIv[256], Rv[256], fv[256];
     double (*sfv)[MAXS] = (double (*)[MAXS])malloc((size_t)N * sizeof(double[MAXS]));
     double (*efv)[MAXS] = (double (*)[MAXS])malloc((size_t)N * sizeof(double[MAXS]));
+    double (*oev)[MAXS] = (double (*)[MAXS])malloc((size_t)N * sizeof(double[MAXS]));
     double *IIa = N <= 256 ? IIv : (double *)malloc((size_t)N * sizeof(double));
     double *Ra = N <= 256 ? Rv : (double *)malloc((size_t)N * sizeof(double));
     double *fa = N <= 256 ? fv : (double *)malloc((size_t)N * sizeof(double));
+    double (*tails)[MAXS] = (double (*)[MAXS])malloc((size_t)N * sizeof(double[MAXS]));
 
     while (i < nI || j < nT) {
         if (++iters > 2 * (nI + nT) + 2) { status = ORC_EBUDGET; break; }
         double t_inf = (i < nI) ? arrival[i] : INFINITY;
-        int64_t task;
+        int64_t task, m = 1;            /* the decision places tasks task .. task + m - 1 */
         double now;
         if (t_inf <= r) {               /* ties: inference first ([R-19]) */
             task = i; now = t_inf;
+            if (cb)                     /* Algorithm 3: the batch this request opens */
+                m = continuous_batch(arrival, i, nI, par->cb_cmax, par->cb_tw, j < nT, r, &now);
         } else {
             task = nI + j; now = r;
             /* queue-level deprioritisation (Eq. 4) against the next enqueued
              * inference task; the training task moves behind it ([R-15]). */
             if (par->policy == ORC_LEMIX && par->deprioritize && i < nI &&
-                should_deprioritize(&T, lbk[i], arrival[i])) {
+                should_deprioritize(&T, lbk[i], arrival[i], now, task_w(lbk[task]))) {
                 r = arrival[i];
                 defer[task]++;
                 counters->deferrals++;
@@ -510,7 +604,29 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
         }
         const uint32_t v = lbk[task];
         const int is_train = task_kind(v);
-        const double a = now;           /* dispatch time ([R-2]) */
+        double a = now;                 /* dispatch time ([R-2]) */
+        if (par->policy == ORC_MIXLUF) {
+            /* Mix-LUF's utilisation query takes luf_delay and the scheduler
+             * serves one decision at a time ([R-luf]) */
+            sched_free = MAX(now, sched_free) + par->luf_delay;
+            a = sched_free;
+        }
+
+        /* ---- the unit being placed: one task, or a batch of m requests
+         * ([R-cb]: C_b = sum of the members' C, padded to the longest) ---- */
+        int64_t l_pad = task_len(v), C_b = task_batch(v), W_D = 0;
+        for (int64_t k = 1; k < m; ++k) {
+            if (task_len(lbk[task + k]) > l_pad) l_pad = task_len(lbk[task + k]);
+            C_b += task_batch(lbk[task + k]);
+        }
+        const double w = (double)(C_b * l_pad * l_pad);
+        if (cb && !is_train) {
+            uint32_t mx = 0;
+            for (int64_t k = 0; k < m; ++k) if (out_len[task + k] > mx) mx = out_len[task + k];
+            W_D = decode_work(out_len + task, m, l_pad, (int64_t)mx);
+        }
+        for (int n = 0; n < N; ++n)
+            for (int s = 0; s < S; ++s) tails[n][s] = eta_d(&T, n, s) * (double)W_D;
         path_t *p = &T.path[task];
 
         /* ---- task-level node allocation ---- */
@@ -522,11 +638,11 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
         }
         if (par->policy == ORC_LEMIX) {
             for (int n = 0; n < N; ++n) {
-                compute_idleness(&T, n, v, a, now, &IIa[n], &Ra[n], sfv[n], efv[n]);
+                compute_idleness(&T, n, w, W_D ? tails[n] : NULL, a, now, &IIa[n], &Ra[n], sfv[n], efv[n], oev[n]);
                 const node_t *nd = &T.node[n];
                 double a_last = (nd->last_task >= 0) ? nd->a_last : a;
                 double IP = idleness_profit(IIa[n], S, a, a_last, par->tau);
-                double LC = length_consistency(&T, nd, task_len(v));
+                double LC = length_consistency(&T, nd, (int)l_pad);
                 fa[n] = priority(par, IP, LC, Ra[n]);
                 if (cand) {
                     cand[(step * N + n) * 3 + 0] = IIa[n];
@@ -562,10 +678,23 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
                     if (is_train) best = ninf + (int)(sep_t++ % (N - ninf));
                     else best = (int)(sep_i++ % ninf);
                 }
+            } else if (par->policy == ORC_MIXLUF) {
+                /* lowest average utilisation first ([R-luf]): the
+                 * node whose GPUs have the least busy time committed so far
+                 * (the common denominator S * elapsed time does not change the
+                 * order); ties -> lowest index */
+                best = 0;
+                double ub = INFINITY;
+                for (int n = 0; n < N; ++n) {
+                    double u = 0.0;
+                    for (int s = 0; s < S; ++s) u = u + T.node[n].busy[s];
+                    if (u < ub) { ub = u; best = n; }
+                }
             } else {
                 best = fixed_node[task];
             }
-            compute_idleness(&T, best, v, a, now, &IIa[best], &Ra[best], sfv[best], efv[best]);
+            compute_idleness(&T, best, w, W_D ? tails[best] : NULL, a, now, &IIa[best], &Ra[best], sfv[best],
+                             efv[best], oev[best]);
             if (cand) {
                 cand[(step * N + best) * 3 + 0] = IIa[best];
                 cand[(step * N + best) * 3 + 1] = Ra[best];
@@ -573,23 +702,27 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
             }
         }
 
-        /* ---- commit: the task joins Q^best ---- */
+        /* ---- commit: the task (or batch) joins Q^best ---- */
         node_t *nd = &T.node[best];
-        const double w = task_w(v);
         if (par->mem_enable) {
             /* Algorithm 2: execute (wait-or-drop) and calibrate */
             sm.n_mem_wait += execute_memory_aware(&T, best, v, a, p->sf, p->ef, p->off);
             for (int s = 0; s < S; ++s) {
+                p->oe[s] = p->ef[s];
                 sm.n_offload += p->off[s];
                 const double dF = eta_f(&T, best, s) * w;
                 const double dur = p->off[s] ? dF + par->mem_pen * (double)((int64_t)task_batch(v) * task_len(v)) : dF;
                 nd->busy[s] = nd->busy[s] + dur;
             }
         } else {
-            for (int s = 0; s < S; ++s) { p->sf[s] = sfv[best][s]; p->ef[s] = efv[best][s]; p->off[s] = 0; }
-            for (int s = 0; s < S; ++s) nd->busy[s] = nd->busy[s] + eta_f(&T, best, s) * w;
+            for (int s = 0; s < S; ++s) {
+                p->sf[s] = sfv[best][s]; p->ef[s] = efv[best][s]; p->oe[s] = oev[best][s]; p->off[s] = 0;
+            }
+            /* busy: the prefill (or forward), then the decode steps that follow it */
+            for (int s = 0; s < S; ++s) nd->busy[s] = (nd->busy[s] + eta_f(&T, best, s) * w) + tails[best][s];
         }
-        double done;
+        double done = 0.0;
+        int64_t ver = 0;
         if (is_train) {
             if (nd->q_len >= par->qcap) { status = ORC_EQCAP; break; }
             plan_backward(&T, best, v, p);
@@ -600,10 +733,6 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
             counters->commits_train++;
             done = p->eb[0];
         } else {
-            done = p->ef[S - 1];
-            double ttft = p->ef[S - 1] - arrival[task];       /* TTFT = R from arrival */
-            sm.sum_ttft = sm.sum_ttft + ttft;
-            if (ttft <= tau_R(&T, v)) sm.n_slo_met++;
             /* version-at-inference: training tasks on this node whose backward
              * (stage 1) ended by this task's forward start. */
             int64_t pending = 0;
@@ -617,31 +746,55 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
                 int64_t kmax = 0;
                 for (int64_t k = 0; k < n_ck; ++k)
                     if (ck_avail[k] <= p->sf[0] && k + 1 > kmax) kmax = k + 1;
-                sm.sum_version += kmax * par->sync_interval;
+                ver = kmax * par->sync_interval;
             } else {
-                sm.sum_version += nd->n_train_on - pending;
+                ver = nd->n_train_on - pending;
             }
+            if (cb) sm.n_batches++;
         }
-        nd->last_task = task;
-        nd->a_last = a;
-        if (!nd->has_efS || p->ef[S - 1] > nd->max_efS) nd->max_efS = p->ef[S - 1];
-        nd->has_efS = 1;
-        nd->hist_cnt += 1;
-        nd->hist_sum += task_len(v);
-        nd->hist_sumsq += (int64_t)task_len(v) * task_len(v);
-        t_last = MAX(t_last, done);
-
-        if (node_defer) node_defer[task] = (uint32_t)best | ((defer[task] > 0xFFFFu ? 0xFFFFu : defer[task]) << 16);
-        if (decision_idx) decision_idx[task] = (int32_t)step;
-        if (completion) completion[task] = done;
-        if (start_f1) start_f1[task] = p->sf[0];
-        if (paths)
-            for (int s = 0; s < S; ++s) {
-                paths[(task * S + s) * 4 + 0] = p->sf[s];
-                paths[(task * S + s) * 4 + 1] = p->ef[s];
-                paths[(task * S + s) * 4 + 2] = is_train ? p->sb[s] : 0.0;
-                paths[(task * S + s) * 4 + 3] = is_train ? p->eb[s] : 0.0;
+        /* per member (one for a single task): completion, TTFT / SLO, TBT */
+        for (int64_t k = 0; k < m; ++k) {
+            const int64_t tk = task + k;
+            if (k > 0) T.path[tk] = *p;                          /* the batch's path */
+            double fin = done;
+            if (!is_train) {
+                fin = p->ef[S - 1];                              /* first token (prefill end) */
+                double ttft = p->ef[S - 1] - arrival[tk];        /* TTFT = R from arrival */
+                sm.sum_ttft = sm.sum_ttft + ttft;
+                if (ttft <= tau_R(&T, lbk[tk])) sm.n_slo_met++;
+                sm.sum_version += ver;
+                if (cb) {
+                    /* its last token: after decode steps 1 .. out on GPU (best, S) */
+                    const int64_t o = (int64_t)out_len[tk];
+                    const double dec = eta_d(&T, best, S - 1) * (double)decode_work(out_len + task, m, l_pad, o);
+                    fin = p->ef[S - 1] + dec;
+                    if (o >= 1) {                                /* TBT: mean gap between its tokens */
+                        sm.sum_tbt = sm.sum_tbt + dec / (double)o;
+                        sm.n_tbt++;
+                    }
+                }
             }
+            t_last = MAX(t_last, fin);
+            if (node_defer) node_defer[tk] = (uint32_t)best | ((defer[tk] > 0xFFFFu ? 0xFFFFu : defer[tk]) << 16);
+            if (decision_idx) decision_idx[tk] = (int32_t)step;
+            if (completion) completion[tk] = fin;
+            if (start_f1) start_f1[tk] = p->sf[0];
+            if (paths)
+                for (int s = 0; s < S; ++s) {
+                    paths[(tk * S + s) * 4 + 0] = p->sf[s];
+                    paths[(tk * S + s) * 4 + 1] = p->ef[s];
+                    paths[(tk * S + s) * 4 + 2] = is_train ? p->sb[s] : 0.0;
+                    paths[(tk * S + s) * 4 + 3] = is_train ? p->eb[s] : 0.0;
+                }
+            /* Eq. 2 history: the lengths of every task run on the node ([R-10]) */
+            nd->hist_cnt += 1;
+            nd->hist_sum += task_len(lbk[tk]);
+            nd->hist_sumsq += (int64_t)task_len(lbk[tk]) * task_len(lbk[tk]);
+        }
+        nd->last_task = task + m - 1;
+        nd->a_last = a;
+        if (!nd->has_efS || p->oe[S - 1] > nd->max_efS) nd->max_efS = p->oe[S - 1];
+        nd->has_efS = 1;
         step++;
         counters->decisions++;
         if (is_train) {
@@ -650,7 +803,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
                 ck_avail[n_ck++] = p->eb[0] + par->sync_latency;
             r = (j < nT) ? MAX(arrival[nI + j], p->ef[0]) : INFINITY;   /* PAPER.md:224 */
         } else {
-            i++;
+            i += m;
         }
     }
 
@@ -663,6 +816,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
         sm.throughput = (sm.makespan > 0.0) ? (double)n_tasks / sm.makespan : 0.0;
         sm.mean_ttft = (nI > 0) ? sm.sum_ttft / (double)nI : 0.0;
         sm.slo_attainment = (nI > 0) ? (double)sm.n_slo_met / (double)nI : 1.0;
+        sm.mean_tbt = (sm.n_tbt > 0) ? sm.sum_tbt / (double)sm.n_tbt : 0.0;
         double U = 0.0, stds = 0.0;
         for (int n = 0; n < N; ++n) {
             for (int s = 0; s < S; ++s) U = U + T.node[n].busy[s];
@@ -685,7 +839,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
     if (summary) *summary = sm;
 
     if (IIa != IIv) { free(IIa); free(Ra); free(fa); }
-    free(sfv); free(efv);
+    free(sfv); free(efv); free(oev); free(tails);
     for (int n = 0; n < N; ++n) free(T.node[n].q_train);
     free(T.node); free(T.path); free(defer); free(ck_avail);
     return status;
@@ -693,14 +847,14 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 
 int orc_run_batch(const orc_profile *prof, const orc_params *par,
                   int64_t n_traces, const int64_t *offsets, const int32_t *n_inf,
-                  const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
+                  const double *arrival, const uint32_t *lbk, const uint32_t *out_len, const int32_t *fixed_node,
                   uint32_t *node_defer, int32_t *decision_idx, double *completion,
                   double *start_f1, orc_summary *summaries, orc_counters *counters)
 {
     int first_err = ORC_OK;
     for (int64_t t = 0; t < n_traces; ++t) {
         int64_t o = offsets[t], n = offsets[t + 1] - offsets[t];
-        int st = orc_run_trace(prof, par, n, n_inf[t], arrival + o, lbk + o,
+        int st = orc_run_trace(prof, par, n, n_inf[t], arrival + o, lbk + o, out_len ? out_len + o : NULL,
                                fixed_node ? fixed_node + o : NULL,
                                node_defer ? node_defer + o : NULL,
                                decision_idx ? decision_idx + o : NULL,

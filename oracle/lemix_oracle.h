@@ -18,7 +18,7 @@
 extern "C" {
 #endif
 
-enum { ORC_LEMIX = 0, ORC_RR = 1, ORC_SEPARATE = 2, ORC_FIXED = 3 };
+enum { ORC_LEMIX = 0, ORC_RR = 1, ORC_SEPARATE = 2, ORC_FIXED = 3, ORC_MIXLUF = 4 };
 enum { ORC_OK = 0, ORC_EINVAL = 1, ORC_EQCAP = 6, ORC_EBUDGET = 7 };
 
 typedef struct {
@@ -26,6 +26,8 @@ typedef struct {
     int32_t n_stages;      /* S (GPUs per node) */
     const double *eta_f;   /* [N*S] node-major: eta_F^n for stage s */
     const double *eta_b;   /* [N*S] node-major: eta_B^n for stage s */
+    const double *eta_d;   /* [N*S] node-major: decode step cost eta_D^n per context token,
+                              or NULL (no decode; only read with continuous batching) */
 } orc_profile;
 
 typedef struct {
@@ -60,13 +62,24 @@ typedef struct {
     int32_t sep_pad;
     double dyn_rate;                /* requests/s threshold (50 in the paper) */
     double dyn_window;              /* seconds */
+    /* Algorithm 3 ContinuousBatching + hybrid prefill/decode (
+     * SURVEY.md §8f NEXT-2; reading R-cb).  cb_cmax = 0: every
+     * request is its own task (the hot-path model). */
+    int32_t cb_cmax;                /* maximum batch size C (requests) */
+    int32_t eq4_mode;               /* Eq. 4 reading: 0 = R-14 (default), 1 = R-14b */
+    double cb_tw;                   /* maximum waiting time T_w, seconds */
+    /* Mix-LUF (reading R-luf): per-decision
+     * scheduler latency (utilisation query), seconds, serialised */
+    double luf_delay;
 } orc_params;
 
 /* Per-trace summary.  Integer block then fp64 block. */
 typedef struct {
     int64_t n_tasks, n_inf, n_train, n_slo_met, n_deferrals, active_nodes, sum_version, status;
     int64_t n_mem_wait, n_offload;  /* stage forwards that waited for memory / were offloaded (Alg. 2) */
+    int64_t n_batches, n_tbt;       /* Alg. 3: inference batches; requests with >= 1 decode step (TBT defined) */
     double makespan, throughput, sum_ttft, mean_ttft, slo_attainment, mean_util, mean_len_std;
+    double sum_tbt, mean_tbt;       /* Alg. 3: time-between-tokens */
 } orc_summary;
 
 /* Event counters used to derive algorithmic fp64 op counts. */
@@ -80,7 +93,10 @@ typedef struct {
  * Run one trace.  Tasks are [0, n_tasks): the first n_inf are inference tasks
  * (non-decreasing arrival), the rest training tasks in release order
  * (arrival = earliest release a_min).  lbk packs l (bits 0-11), C (bits 12-19),
- * kind (bit 20, 1 = training).
+ * kind (bit 20, 1 = training).  out_len[n_tasks] = decode steps (tokens after
+ * the prefill's first) of an inference request (0..2048; read only with
+ * continuous batching; may be NULL otherwise).  With continuous batching an inference task's completion is the
+ * time of its last token.
  *
  * Outputs (any may be NULL): node_defer[n_tasks] = node | deferrals<<16;
  * decision_idx[n_tasks]; completion[n_tasks] (inference end_f^S, training
@@ -91,7 +107,7 @@ typedef struct {
  */
 int orc_run_trace(const orc_profile *prof, const orc_params *par,
                   int64_t n_tasks, int64_t n_inf,
-                  const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
+                  const double *arrival, const uint32_t *lbk, const uint32_t *out_len, const int32_t *fixed_node,
                   uint32_t *node_defer, int32_t *decision_idx, double *completion,
                   double *start_f1, double *paths, double *cand,
                   orc_summary *summary, orc_counters *counters);
@@ -99,7 +115,7 @@ int orc_run_trace(const orc_profile *prof, const orc_params *par,
 /* Loop of orc_run_trace over a CSR batch of traces (offsets[n_traces+1], n_inf[n_traces]). */
 int orc_run_batch(const orc_profile *prof, const orc_params *par,
                   int64_t n_traces, const int64_t *offsets, const int32_t *n_inf,
-                  const double *arrival, const uint32_t *lbk, const int32_t *fixed_node,
+                  const double *arrival, const uint32_t *lbk, const uint32_t *out_len, const int32_t *fixed_node,
                   uint32_t *node_defer, int32_t *decision_idx, double *completion,
                   double *start_f1, orc_summary *summaries, orc_counters *counters);
 

@@ -73,6 +73,7 @@ const char *field_name(int code)
     case lmx::kErrOrder: return "arrival (inference tasks must be non-decreasing)";
     case lmx::kErrFixed: return "fixed_node (must be in [0, n_nodes))";
     case lmx::kErrSeparateN1: return "policy Separate needs n_nodes >= 2 when both kinds are present";
+    case lmx::kErrOutLen: return "out_len (must be 0..2048)";
     case lmx::kErrResponse: return "profile/arrival: a candidate's response time R <= 0 (Eq. 3 undefined; eta too small for the arrival time)";
     default: return "unknown";
     }
@@ -141,8 +142,8 @@ struct lmx_ctx {
     int64_t h_seq_len = 0;
     std::vector<int64_t> h_offsets;
     std::vector<int32_t> h_n_inf;
-    bool has_fixed = false;
-    DevBuf offsets, n_inf, arrival, lbk, fixed;
+    bool has_fixed = false, has_out_len = false;
+    DevBuf offsets, n_inf, arrival, lbk, fixed, out_len;
 
     // params
     bool have_params = false;
@@ -213,6 +214,10 @@ void lmx_params_default(lmx_params *p)
     p->dyn_window = 10.0;
     p->debug_level = 0;
     p->debug_pad = 0;
+    p->cb_cmax = 0;        // every request placed on its own
+    p->eq4_mode = 0;       // R-14
+    p->cb_tw = 0.0;
+    p->luf_delay = 0.0;
 }
 
 lmx_status lmx_create(lmx_ctx **out, int device, void *cuda_stream)
@@ -293,7 +298,8 @@ lmx_status lmx_load_profile(lmx_ctx *c, const lmx_profile *pr)
     if (pr->n_stages < 1 || pr->n_stages > 16)
         return c->fail(LMX_EINVAL, "profile.n_stages must be in [1, 16], got " + std::to_string(pr->n_stages));
     const int NS = pr->n_nodes * pr->n_stages;
-    std::vector<double> h(2 * (size_t)NS);
+    // eta_f | eta_b | eta_d (+ one pad double: the kernel stages a multiple of 16 bytes)
+    std::vector<double> h(3 * (size_t)NS + 1, 0.0);
     for (int k = 0; k < NS; ++k) {
         const double f = pr->eta_f[k], b = pr->eta_b[k];
         if (!(f > 0.0 && std::isfinite(f)))
@@ -302,6 +308,12 @@ lmx_status lmx_load_profile(lmx_ctx *c, const lmx_profile *pr)
             return c->fail(LMX_EINVAL, "profile.eta_b[" + std::to_string(k) + "] must be finite and > 0");
         h[k] = f;
         h[NS + k] = b;
+        if (pr->eta_d) {
+            const double d = pr->eta_d[k];
+            if (!(d >= 0.0 && std::isfinite(d)))
+                return c->fail(LMX_EINVAL, "profile.eta_d[" + std::to_string(k) + "] must be finite and >= 0");
+            h[2 * NS + k] = d;
+        }
     }
     cudaSetDevice(c->device);
     if (c->eta.ensure(h.size() * sizeof(double)) != cudaSuccess) return c->fail(LMX_ENOMEM, "profile allocation");
@@ -350,11 +362,23 @@ lmx_status lmx_load_traces(lmx_ctx *c, const lmx_traces *tr, lmx_mem mem)
                     "n_inf copy");
     if (s != LMX_OK) return s;
     c->has_fixed = tr->fixed_node != nullptr;
+    c->has_out_len = tr->out_len != nullptr;
     if (mem == LMX_DEVICE) {
         c->arrival.borrow(tr->arrival);
         c->lbk.borrow(tr->len_batch_kind);
         if (c->has_fixed) c->fixed.borrow(tr->fixed_node);
+        if (c->has_out_len) c->out_len.borrow(tr->out_len);
     } else {
+        if (c->has_out_len) {   // decode lengths (continuous batching): copied here, not streamed
+            if (c->out_len.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess)
+                return c->fail(LMX_ENOMEM, "out_len allocation");
+            if (M > 0) {
+                s = c->cuda(cudaMemcpyAsync(c->out_len.p, tr->out_len, M * 4, cudaMemcpyHostToDevice, c->stream),
+                            "out_len copy");
+                if (s == LMX_OK) s = c->cuda(cudaStreamSynchronize(c->stream), "out_len copy");
+                if (s != LMX_OK) return s;
+            }
+        }
         if (c->arrival.ensure(std::max<int64_t>(M, 1) * 8) != cudaSuccess ||
             c->lbk.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess ||
             (c->has_fixed && c->fixed.ensure(std::max<int64_t>(M, 1) * 4) != cudaSuccess))
@@ -383,7 +407,15 @@ lmx_status lmx_set_params(lmx_ctx *c, const lmx_params *p)
 {
     if (!c) return LMX_EINVAL;
     if (!p) return c->fail(LMX_EINVAL, "lmx_set_params: NULL params");
-    if (p->policy < LMX_LEMIX || p->policy > LMX_FIXED) return c->fail(LMX_EINVAL, "params.policy out of range");
+    if (p->policy < LMX_LEMIX || p->policy > LMX_MIXLUF) return c->fail(LMX_EINVAL, "params.policy out of range");
+    if (p->cb_cmax < 0 || p->cb_cmax > 4096) return c->fail(LMX_EINVAL, "params.cb_cmax must be in [0, 4096]");
+    if (p->cb_cmax > 0 && !(p->cb_tw >= 0.0 && std::isfinite(p->cb_tw)))
+        return c->fail(LMX_EINVAL, "params.cb_tw must be finite and >= 0");
+    if (p->cb_cmax > 0 && p->mem_enable)
+        return c->fail(LMX_EINVAL, "params.cb_cmax: continuous batching is not combined with mem_enable");
+    if (p->eq4_mode != 0 && p->eq4_mode != 1) return c->fail(LMX_EINVAL, "params.eq4_mode must be 0 or 1");
+    if (!(p->luf_delay >= 0.0 && std::isfinite(p->luf_delay)))
+        return c->fail(LMX_EINVAL, "params.luf_delay must be finite and >= 0");
     if (p->deprioritize != 0 && p->deprioritize != 1) return c->fail(LMX_EINVAL, "params.deprioritize must be 0 or 1");
     if (p->slo_mode != 0 && p->slo_mode != 1) return c->fail(LMX_EINVAL, "params.slo_mode must be 0 or 1");
     if (p->qcap < 1 || p->qcap > 65536) return c->fail(LMX_EINVAL, "params.qcap must be in [1, 65536]");
@@ -506,6 +538,8 @@ lmx_status lmx_run(lmx_ctx *c)
     const lmx_params &P = c->par;
     if (P.policy == LMX_FIXED && !c->has_fixed)
         return c->fail(LMX_EINVAL, "policy LMX_FIXED needs traces.fixed_node");
+    if (P.cb_cmax > 0 && !c->has_out_len)
+        return c->fail(LMX_EINVAL, "continuous batching (params.cb_cmax > 0) needs traces.out_len");
     cudaSetDevice(c->device);
     const int64_t T = c->n_traces, M = c->n_tasks;
 
@@ -558,6 +592,11 @@ lmx_status lmx_run(lmx_ctx *c)
     k.sep_dynamic = (P.policy == LMX_SEPARATE && P.sep_dynamic) ? 1 : 0;
     k.dyn_rate = P.dyn_rate;
     k.dyn_window = P.dyn_window;
+    k.cb_cmax = P.cb_cmax;
+    k.cb_tw = P.cb_tw;
+    k.eq4_mode = P.eq4_mode;
+    k.luf_delay = P.luf_delay;
+    k.out_len = c->has_out_len ? (const uint32_t *)c->out_len.p : nullptr;
     if (c->n_cell_par > 0) {
         if (!c->cells_set || c->n_cells != c->n_cell_par)
             return c->fail(LMX_ESTATE, "lmx_run: cell params need lmx_set_cells with the same n_cells");

@@ -38,6 +38,11 @@ struct KParams {
     double dyn_rate, dyn_window;
     double *ck;
     int32_t ck_cap;
+    // Algorithm 3 continuous batching (lmx_params.cb_*; MODE 2 instantiations),
+    // Eq. 4 reading, Mix-LUF scheduler latency
+    int32_t cb_cmax, eq4_mode;
+    double cb_tw, luf_delay;
+    const uint32_t *out_len;   // device [n_tasks] decode steps, or nullptr
     // per-cell (lambda1, lambda2, tau) of lmx_set_cell_params, or nullptr
     const double *cell_par;
     const int32_t *cell_of;
@@ -48,7 +53,7 @@ struct KParams {
     const double *arrival;     // device [n_tasks]
     const uint32_t *lbk;       // device [n_tasks]
     const int32_t *fixed;      // device [n_tasks] or nullptr
-    const double *eta;         // device [2*N*S]: eta_f then eta_b, node-major
+    const double *eta;         // device [3*N*S + 1]: eta_f, eta_b, eta_d node-major (+ pad)
     // streamed inputs (lmx_run with host traces): chunks of chunk_tasks tasks
     // land in order; *ready = number of chunks copied (nullptr: all resident)
     const unsigned *ready;
@@ -72,7 +77,7 @@ struct KParams {
 // field codes for trace_err (reported by lmx_last_error)
 enum : int32_t {
     kErrNone = 0, kErrLen = 1, kErrBatch = 2, kErrKind = 3, kErrBits = 4, kErrArrival = 5,
-    kErrOrder = 6, kErrFixed = 7, kErrSeparateN1 = 8, kErrResponse = 9
+    kErrOrder = 6, kErrFixed = 7, kErrSeparateN1 = 8, kErrResponse = 9, kErrOutLen = 10
 };
 
 struct CellParams {

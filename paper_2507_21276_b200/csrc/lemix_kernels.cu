@@ -93,12 +93,15 @@ kernel_fn pick_tile_lemix(const KParams &p);
 kernel_fn pick_tile_base(const KParams &p);
 kernel_fn pick_tile_lemix_mem(const KParams &p);
 kernel_fn pick_tile_base_mem(const KParams &p);
+kernel_fn pick_tile_lemix_cb(const KParams &p);
+kernel_fn pick_tile_base_cb(const KParams &p);
 
 namespace {
 
 kernel_fn pick(const KParams &p)
 {
     if (p.mem_enable) return p.policy == LMX_LEMIX ? pick_tile_lemix_mem(p) : pick_tile_base_mem(p);
+    if (p.cb_cmax > 0) return p.policy == LMX_LEMIX ? pick_tile_lemix_cb(p) : pick_tile_base_cb(p);
     return p.policy == LMX_LEMIX ? pick_tile_lemix(p) : pick_tile_base(p);
 }
 
@@ -112,7 +115,7 @@ int event_loop_smem_bytes(const KParams &p)
 {
     const int W = tile::window_entries(p.S);
     const int npl = npl_bucket(p.npl);
-    return 16 * p.N * p.S + (W > 0 ? kBlock * npl * W * ring_words(p.S, p.mem_enable != 0) * 16 : 0) +
+    return (int)tile::profile_bytes(p.N * p.S, p.cb_cmax > 0) + (W > 0 ? kBlock * npl * W * ring_words(p.S, p.mem_enable != 0) * 16 : 0) +
            kBlock * (npl * tile::cold_words(p.S, npl > 1) + (p.cell_par ? tile::kTraceWords : 4)) * 8;
 }
 

@@ -60,17 +60,27 @@ using dev::task_w;
 inline int stages_bucket(int S) { return S <= 1 ? 1 : S <= 2 ? 2 : S <= 4 ? 4 : S <= 8 ? 8 : 16; }
 inline int npl_bucket(int npl) { return npl <= 1 ? 1 : npl <= 2 ? 2 : 4; }
 inline int window_entries(int S) { return stages_bucket(S) <= 2 ? LMX_TILE_WIN : 0; }
+// bytes of the TMA-staged profile: eta_f | eta_b, plus eta_d with continuous
+// batching, rounded up to the bulk copy's 16-byte granule
+__host__ __device__ inline uint32_t profile_bytes(int NS, bool cb) { return cb ? (24u * NS + 15u) & ~15u : 16u * NS; }
 // 8-byte shared-memory words of commit-only state per node slot and thread
 // (+ 4 words of scoring state when a lane owns several nodes, see SCOLD)
 __host__ __device__ inline int cold_words(int S, bool scold) { return 2 * S + 4 + (scold ? 4 : 0); }
 
-template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, bool MEM>
+// MODE of an instantiation: 0 the hot-path model; 1 Algorithm 2 memory-aware
+// execution (NEXT-1); 2 Algorithm 3 continuous batching + decode (NEXT-2)
+enum : int { kPlain = 0, kMem = 1, kCb = 2 };
+
+template <int SMAX, bool EXACT, int NPL, bool LEMIX, int TT, int MODE>
 __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_MINB) event_loop_kernel(const KParams p)
 {
     // LEMIX: the policy is LeMix (all candidates planned and scored); else one
-    // of the baselines (RR / Separate / Fixed) picks the node first.
+    // of the baselines (RR / Separate / Fixed / Mix-LUF) picks the node first.
     // MEM: the committed task is executed under Algorithm 2's memory model
     // (dev::execute_mem) and the executed path replaces the plan.
+    // CB: inference requests are batched (Algorithm 3, DESIGN.md R-cb) and
+    // each batch's decode steps occupy its node after the prefill.
+    constexpr bool MEM = MODE == kMem, CB = MODE == kCb;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t s_bar;
 
@@ -81,11 +91,12 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     // LeMix instantiations; the host picks one of those when they are set
     constexpr bool CPAR = LEMIX && TT == 0;
 
-    // ---- K1: stage eta_f | eta_b (16*N*S bytes) into shared memory via TMA ----
+    // ---- K1: stage eta_f | eta_b (| eta_d) into shared memory via TMA ----
+    const uint32_t pbytes = profile_bytes(NS, CB);
     if (threadIdx.x == 0) {
         dev::mbar_init(&s_bar, 1);
-        dev::mbar_arrive_expect_tx(&s_bar, 16u * (uint32_t)NS);
-        dev::bulk_copy_g2s(s_eta, p.eta, 16u * (uint32_t)NS, &s_bar);
+        dev::mbar_arrive_expect_tx(&s_bar, pbytes);
+        dev::bulk_copy_g2s(s_eta, p.eta, pbytes, &s_bar);
     }
     __syncthreads();
     dev::mbar_wait(&s_bar, 0);
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     double2 *rbe[NPL];
 #pragma unroll
     for (int jj = 0; jj < NPL; ++jj) {
-        ws[jj] = dev::smem_u32(smem_raw + 16 * NS) + (uint32_t)(jj * (W > 0 ? W : 1) * ring_words(S, MEM)) * wstride +
+        ws[jj] = dev::smem_u32(smem_raw + pbytes) + (uint32_t)(jj * (W > 0 ? W : 1) * ring_words(S, MEM)) * wstride +
                  16u * threadIdx.x;
         dev::opaque(ws[jj]);   // keep in a register: no per-iteration rematerialisation
         const long long rbase = (gtile * p.npad + (tl + jj * T)) * K;
@@ -128,7 +139,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     constexpr uint32_t cstride = 8u * kBlock;   // (blockDim.x == kBlock): immediate offsets
     constexpr bool SCOLD = NPL > 1;
     const int CW = cold_words(S, SCOLD);   // words per node slot
-    uint32_t cbase = dev::smem_u32(smem_raw + 16 * NS) +
+    uint32_t cbase = dev::smem_u32(smem_raw + pbytes) +
                      (uint32_t)(W > 0 ? NPL * W * ring_words(S, MEM) : 0) * wstride + 8u * threadIdx.x;
     dev::opaque(cbase);
     auto c_lb = [&](int jj, int s) { return cbase + (uint32_t)(jj * CW + s) * cstride; };
@@ -159,6 +170,9 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
     int n_slo = 0, n_def = 0;             // (<= 2^19 tasks, <= 2^20 decisions per trace)
     int n_mwait = 0, n_moff = 0;          // Algorithm 2 counters (MEM)
     int n_ck = 0;                         // Separate's checkpoints so far (sync model)
+    int n_batches = 0, n_tbt = 0;         // Algorithm 3 (CB): batches placed, requests with decode steps
+    double sum_tbt = 0.0;
+    double sched_free = -kInf;            // Mix-LUF: when the scheduler's previous query ends (R-luf)
     double *ckt = (!LEMIX && p.sync_sep) ? p.ck + gtile * p.ck_cap : nullptr;
     double a_inf = 0.0, a_inf2 = 0.0, a_tr = 0.0, a_tr2 = 0.0;   // 2-deep input prefetch
     uint32_t v_inf = 0, v_inf2 = 0, v_tr = 0, v_tr2 = 0;
@@ -198,6 +212,9 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 n_slo = sum_ver = n_def = 0;
                 n_mwait = n_moff = 0;
                 n_ck = 0;
+                n_batches = n_tbt = 0;
+                sum_tbt = 0.0;
+                sched_free = -kInf;
                 sum_ttft = 0.0;
                 t_last = -kInf;
                 a_last_inf = -kInf;
@@ -262,9 +279,9 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
             sm.n_train = nT;
             sm.status = status;
             sm.n_slo_met = sm.n_deferrals = sm.active_nodes = sm.sum_version = 0;
-            sm.n_mem_wait = sm.n_offload = 0;
+            sm.n_mem_wait = sm.n_offload = sm.n_batches = sm.n_tbt = 0;
             sm.makespan = sm.throughput = sm.sum_ttft = sm.mean_ttft = sm.slo_attainment = 0.0;
-            sm.mean_util = sm.mean_len_std = 0.0;
+            sm.mean_util = sm.mean_len_std = sm.sum_tbt = sm.mean_tbt = 0.0;
             if (status == LMX_OK) {
                 const int ntask = nI + nT;
                 sm.n_slo_met = n_slo;
@@ -272,6 +289,10 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 sm.sum_version = sum_ver;
                 sm.n_mem_wait = n_mwait;
                 sm.n_offload = n_moff;
+                sm.n_batches = n_batches;
+                sm.n_tbt = n_tbt;
+                sm.sum_tbt = sum_tbt;
+                sm.mean_tbt = (n_tbt > 0) ? sum_tbt / (double)n_tbt : 0.0;
                 sm.sum_ttft = sum_ttft;
                 sm.makespan = (ntask > 0) ? t_last - dev::lds_d(c_tw(2)) : 0.0;
                 sm.throughput = (sm.makespan > 0.0) ? (double)ntask / sm.makespan : 0.0;
@@ -327,8 +348,41 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
 #endif
             const double t_inf = (i < nI) ? a_inf : kInf;
             const bool is_train = !(t_inf <= r);
-            const double now = is_train ? r : t_inf;
+            double now = is_train ? r : t_inf;
             const uint32_t v = is_train ? v_tr : v_inf;
+            // CB: the unit placed is the batch request i opens (Algorithm 3,
+            // PAPER.md:693-716; DESIGN.md R-cb): members i .. i + mb - 1, C_b
+            // items padded to length lpad, decode work wd (exact token units)
+            int mb = 1, lpad = task_len(v), cb_err = 0;
+            long long cbt = task_batch(v), wd = 0, sum_l = task_len(v), sum_l2 = (long long)task_len(v) * task_len(v);
+            if (CB && live && !is_train) {
+                // lines 7-12: join while not full, not behind a released training
+                // task (ties -> inference) and before the timer T_start + T_w
+                while (i + mb < nI && mb < p.cb_cmax) {
+                    const double ar = __ldg(tarr + i + mb);
+                    if ((j < nT && r < ar) || !(t_inf + p.cb_tw > ar)) break;
+                    const uint32_t vm = __ldg(tlbk + i + mb);
+                    const unsigned lm = (unsigned)task_len(vm);
+                    if (!(((vm >> 21) == 0u) & (lm - 1u < 2048u) & (task_batch(vm) >= 1) & (((vm >> 20) & 1u) == 0u) &
+                          (ar < kInf) & (ar >= __ldg(tarr + i + mb - 1))))
+                        cb_err = 1;   // (reported as the member's own field error below)
+                    lpad = max(lpad, (int)lm);
+                    cbt += task_batch(vm);
+                    sum_l += lm;
+                    sum_l2 += (long long)lm * lm;
+                    mb++;
+                }
+                // line 15: full -> at the C-th arrival, else the timer or the training release
+                now = (mb == p.cb_cmax) ? __ldg(tarr + i + mb - 1) : dev::dmin(t_inf + p.cb_tw, (j < nT) ? r : kInf);
+                // decode steps 1 .. out_j of every member over the padded context
+                // (SPEC.md:410): sum_j g(out_j), g(o) = o (lpad - 1) + o (o + 1) / 2
+                const long long o0 = dev::lds_l(c_tw(1)) + i;
+                for (int k = 0; k < mb; ++k) {
+                    const long long ok = __ldg(p.out_len + o0 + k);
+                    if (ok > 2048) cb_err = 2;
+                    wd += ok * (lpad - 1) + ok * (ok + 1) / 2;
+                }
+            }
             // Inputs two ahead in the stream this decision consumes, loaded
             // now so they land while the decision runs (loaded at its end, the
             // loop-carried register copies at the top of the next iteration
@@ -349,7 +403,17 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 for (int jj = 0; jj < NPL; ++jj) {
                     const int n = tl + jj * T;
                     if (n < N) {
-                        const double latest = hasp[jj] ? dev::last_of(P[jj], S) : -kInf;
+                        double latest = hasp[jj] ? dev::last_of(P[jj], S) : -kInf;
+                        if (p.eq4_mode == 1) {
+                            // R-14b: the training task's own forward, chained stage by
+                            // stage after the node's last forward, comes first
+                            const double wt = task_w(v);
+                            double vv = now;
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) vv = dev::dmax(vv, hasp[jj] ? P[jj][s] : -kInf) + prof.f(n, s) * wt;
+                            latest = vv;
+                        }
                         m = dev::dmin(m, latest + prof.f(n, S - 1) * wn);
                     }
                 }
@@ -388,6 +452,10 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                     fx = __ldg(p.fixed + dev::lds_l(c_tw(1)) + task);
                     ok = ok & (fx >= 0) & (fx < N);
                 }
+                if (CB && cb_err) {
+                    status = LMX_EINVAL;
+                    dev::sts_l(c_tw(3), ((long long)task << 8) | (cb_err == 2 ? kErrOutLen : kErrBits));
+                }
                 if (!ok) {
                     int code = kErrFixed;
                     if (v >> 21) code = kErrBits;
@@ -402,9 +470,11 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
             }
             const bool place = live && !deferred && status == LMX_OK;   // this tile places a task
             {
-                const double a = now;                    // dispatch time (R-2)
-                const double w = task_w(v);
-                const int l = task_len(v);
+                double a = now;                          // dispatch time (R-2)
+                // the unit's C*l^2 (a batch: its items, padded, R-cb) and the
+                // length Eq. 2 scores
+                const double w = CB ? (double)(cbt * lpad * lpad) : task_w(v);
+                const int l = CB ? lpad : task_len(v);
 
                 // ---- a9: baseline selectors ----
                 int chosen = -1;
@@ -428,12 +498,30 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                         }
                         chosen = is_train ? ninf + (sep_t++ % (N - ninf)) : (sep_i++ % ninf);
                     }
+                } else if (p.policy == LMX_MIXLUF) {
+                    // Mix-LUF (R-luf): the node with the least busy
+                    // time committed so far (busy columns of the tile's lanes,
+                    // summed stage by stage), lowest index on ties; the decision
+                    // waits for the serialised utilisation query
+                    __syncwarp(tmask);
+                    double ub = kInf;
+                    chosen = 0;
+                    for (int n = 0; n < N; ++n) {
+                        const uint32_t col = 8u * (uint32_t)((n & (T - 1)) - tl);
+                        const int jn = n >> log2T;
+                        double u = 0.0;
+                        for (int s = 0; s < S; ++s) u = u + dev::lds_d(c_busy(0, s) + (uint32_t)(jn * CW) * cstride + col);
+                        if (u < ub) { ub = u; chosen = n; }
+                    }
+                    sched_free = dev::dmax(now, sched_free) + p.luf_delay;
+                    a = sched_free;
                 } else {
                     chosen = __ldg(p.fixed + dev::lds_l(c_tw(1)) + task);
                 }
 
                 // ---- a3-a7: Algorithm 1 + Eq. 1-3 for every candidate this lane owns ----
                 double en_s[NPL][SMAX];
+                double oc_s[NPL][SMAX];   // CB: occupancy ends (forward + the batch's decode steps)
                 double st0_s[NPL];
                 double f_best = 0.0;
                 int n_best = INT_MAX;
@@ -471,8 +559,18 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                         const dev::RingT<W, wstride, MEM> q{rbe[jj], p.kmask, S, ws[jj], wstride, qhead + qlen};
                         double efn[SMAX], ebn[SMAX];
                         prof.node<SMAX>(n, efn, ebn);
-                        dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, efn, ebn, q, qhead, qlen, sk[jj], skeb[jj], w,
-                                        a, now, en_s[jj], st0_s[jj], II, gc);
+                        if (CB) {
+                            // the batch's decode steps follow its prefill on each GPU
+                            double tl_n[SMAX];
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s) tl_n[s] = (s < S) ? prof.d(n, s) * (double)wd : 0.0;
+                            dev::plan<SMAX, LMX_TILE_PF, dev::RingT<W, wstride, MEM>, true>(
+                                P[jj], hasp[jj] != 0, S, efn, ebn, q, qhead, qlen, sk[jj], skeb[jj], w, a, now, en_s[jj],
+                                st0_s[jj], II, gc, &tl_n, &oc_s[jj]);
+                        } else {
+                            dev::plan<SMAX, LMX_TILE_PF>(P[jj], hasp[jj] != 0, S, efn, ebn, q, qhead, qlen, sk[jj], skeb[jj],
+                                                         w, a, now, en_s[jj], st0_s[jj], II, gc);
+                        }
                         // lines 17-18: executed entries leave Q_train^n (a head advance:
                         // end_b^1 is non-decreasing along the queue)
                         qh[jj] = qhead + gc;
@@ -496,10 +594,10 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                             dev::put_cand(p.cand, (dev::lds_l(c_tw(1)) + step) * N + n, II,
                                           dev::last_of(en_s[jj], S) - a, __longlong_as_double(-1ll));
                         }
-                        {   // speculative statistics: count cnt+1, sums + l, + l^2
-                            const long long c = cnt[jj] + 1;
-                            const long long a1 = dev::lds_l(c_sl(jj)) + l;
-                            const long long a2 = dev::lds_l(c_sl2(jj)) + (long long)l * l;
+                        {   // speculative statistics: count + members, sums + their l, l^2
+                            const long long c = cnt[jj] + (CB ? mb : 1);
+                            const long long a1 = dev::lds_l(c_sl(jj)) + (CB ? sum_l : l);
+                            const long long a2 = dev::lds_l(c_sl2(jj)) + (CB ? sum_l2 : (long long)l * l);
                             sl_n[jj] = a1;
                             sl2_n[jj] = a2;
                             const double inv_c = 1.0 / (double)c;
@@ -585,10 +683,11 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
 #pragma unroll
                             for (int s = 0; s < SMAX; ++s)
                                 if (s < S) {
-                                    P[jj][s] = en_s[jj][s];
+                                    P[jj][s] = CB ? oc_s[jj][s] : en_s[jj][s];   // (CB: busy through the decode steps)
                                     const double dFs = ef[s] * w;
                                     const double dur = (MEM && ((offm >> s) & 1)) ? dFs + p.mem_pen * (double)tok : dFs;
                                     bz[s] = dev::lds_d(c_busy(jj, s)) + dur;
+                                    if (CB) bz[s] = bz[s] + prof.d(best, s) * (double)wd;   // the decode steps
                                 }
                             const long long trv = dev::lds_l(c_ntr(jj));
                             int ntr = (int)(trv & 0xffffffffll), vp = (int)(trv >> 32);
@@ -655,7 +754,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                                 // cached Eq. 2 statistics (DESIGN.md R-stat), computed
                                 // speculatively above; unused while cnt < 2.  (Also on a
                                 // queue overflow: that trace stops, its state is dead.)
-                                cnt[jj]++;
+                                cnt[jj] += CB ? mb : 1;
                                 dev::sts_l(c_sl(jj), sl_n[jj]);
                                 dev::sts_l(c_sl2(jj), sl2_n[jj]);
                                 if (SCOLD) {
@@ -682,6 +781,60 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 if (!place_c) {
                 } else if (c_ver == INT_MIN) {
                     status = LMX_EQCAP;
+                } else if (CB && !is_train) {
+                    // ---- a11 for a batch (R-cb): every member's first token at the
+                    // prefill end, its last after its own decode steps; TTFT, SLO,
+                    // TBT per member, in member order ----
+                    const double edS = prof.d(best, S - 1);
+                    const long long o0 = dev::lds_l(c_tw(1)) + i;
+                    for (int k = 0; k < mb; ++k) {
+                        const double ar = __ldg(tarr + i + k);
+                        const uint32_t vk = __ldg(tlbk + i + k);
+                        const long long ok = __ldg(p.out_len + o0 + k);
+                        // decode work up to its last step: sum_j g(min(out_k, out_j))
+                        long long wk = 0;
+                        for (int jm = 0; jm < mb; ++jm) {
+                            const long long oj = __ldg(p.out_len + o0 + jm);
+                            const long long mn = oj < ok ? oj : ok;
+                            wk += mn * (lpad - 1) + mn * (mn + 1) / 2;
+                        }
+                        const double dec = edS * (double)wk;
+                        const double fin = c_done + dec;
+                        const double ttft = c_done - ar;
+                        double tauR;
+                        if (p.slo_mode == 1) {
+                            tauR = p.slo_const;
+                        } else {
+                            const double wk2 = task_w(vk);
+                            double acc = 0.0;
+#pragma unroll
+                            for (int s = 0; s < SMAX; ++s)
+                                if (s < S) acc = acc + ef0[s] * wk2;
+                            tauR = p.slo_mult * acc;
+                        }
+                        sum_ttft = sum_ttft + ttft;
+                        n_slo += (ttft <= tauR) ? 1 : 0;
+                        sum_ver += c_ver;
+                        if (ok >= 1) {
+                            sum_tbt = sum_tbt + dec / (double)ok;
+                            n_tbt++;
+                        }
+                        t_last = dev::dmax(t_last, fin);
+                        if (tl == 0 && p.node_defer) {
+                            p.node_defer[o0 + k] = (uint32_t)best;
+                            p.decision_idx[o0 + k] = step;
+                            p.completion[o0 + k] = fin;
+                            p.start_f1[o0 + k] = c_st0;
+                        }
+                    }
+                    n_batches++;
+                    step++;
+                    a_last_inf = __ldg(tarr + i + mb - 1);
+                    i += mb;
+                    a_inf = (i < nI) ? __ldg(tarr + i) : 0.0;
+                    v_inf = (i < nI) ? __ldg(tlbk + i) : 0u;
+                    a_inf2 = (i + 1 < nI) ? __ldg(tarr + i + 1) : 0.0;
+                    v_inf2 = (i + 1 < nI) ? __ldg(tlbk + i + 1) : 0u;
                 } else {
                     // ---- a11: outputs + per-trace folds ----
                     if (tl == 0 && p.node_defer) {
@@ -697,7 +850,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                     // both kinds' folds as selects (no divergence between tiles
                     // that placed a training and an inference task)
                     const bool inf = !is_train;
-                    const double ttft = c_done - a;            // R from arrival
+                    const double ttft = c_done - a_inf;        // R from arrival
                     double tauR;
                     if (p.slo_mode == 1) {
                         tauR = p.slo_const;
@@ -712,7 +865,7 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                     sum_ttft = inf ? sum_ttft_n : sum_ttft;
                     n_slo += (inf && ttft <= tauR) ? 1 : 0;   // SLO: TTFT <= 5x forward latency
                     sum_ver += inf ? c_ver : 0;
-                    a_last_inf = inf ? a : a_last_inf;
+                    a_last_inf = inf ? a_inf : a_last_inf;
                     i += inf ? 1 : 0;
                     j += inf ? 0 : 1;
                     cur_defer = inf ? cur_defer : 0;
@@ -746,29 +899,29 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
 
 typedef void (*kernel_fn)(const KParams);
 
-template <int SMAX, bool EXACT, bool LEMIX, bool MEM>
+template <int SMAX, bool EXACT, bool LEMIX, int MODE>
 kernel_fn pick_npl(int npl)
 {
     switch (npl) {
-    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX, 0, MEM>;
-    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX, 0, MEM>;
-    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX, 0, MEM>;
+    case 1: return event_loop_kernel<SMAX, EXACT, 1, LEMIX, 0, MODE>;
+    case 2: return event_loop_kernel<SMAX, EXACT, 2, LEMIX, 0, MODE>;
+    default: return event_loop_kernel<SMAX, EXACT, 4, LEMIX, 0, MODE>;
     }
 }
 
-template <bool LEMIX, bool MEM>
+template <bool LEMIX, int MODE>
 kernel_fn pick(const KParams &p)
 {
     const int nb = npl_bucket(p.npl);
     switch (stages_bucket(p.S)) {
-    case 1: return pick_npl<1, true, LEMIX, MEM>(nb);
+    case 1: return pick_npl<1, true, LEMIX, MODE>(nb);
     case 2:
         // the bench shape (4 nodes x 2 stages): tile width fixed at compile time
-        if (p.S == 2 && nb == 1 && p.T == 4 && !p.cell_par) return event_loop_kernel<2, true, 1, LEMIX, 4, MEM>;
-        return p.S == 2 ? pick_npl<2, true, LEMIX, MEM>(nb) : pick_npl<2, false, LEMIX, MEM>(nb);
-    case 4: return p.S == 4 ? pick_npl<4, true, LEMIX, MEM>(nb) : pick_npl<4, false, LEMIX, MEM>(nb);
-    case 8: return p.S == 8 ? pick_npl<8, true, LEMIX, MEM>(nb) : pick_npl<8, false, LEMIX, MEM>(nb);
-    default: return p.S == 16 ? pick_npl<16, true, LEMIX, MEM>(nb) : pick_npl<16, false, LEMIX, MEM>(nb);
+        if (p.S == 2 && nb == 1 && p.T == 4 && !p.cell_par) return event_loop_kernel<2, true, 1, LEMIX, 4, MODE>;
+        return p.S == 2 ? pick_npl<2, true, LEMIX, MODE>(nb) : pick_npl<2, false, LEMIX, MODE>(nb);
+    case 4: return p.S == 4 ? pick_npl<4, true, LEMIX, MODE>(nb) : pick_npl<4, false, LEMIX, MODE>(nb);
+    case 8: return p.S == 8 ? pick_npl<8, true, LEMIX, MODE>(nb) : pick_npl<8, false, LEMIX, MODE>(nb);
+    default: return p.S == 16 ? pick_npl<16, true, LEMIX, MODE>(nb) : pick_npl<16, false, LEMIX, MODE>(nb);
     }
 }
 

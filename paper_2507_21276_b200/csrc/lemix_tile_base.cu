@@ -4,5 +4,5 @@
 
 namespace lmx {
 typedef void (*tile_kernel_fn)(const KParams);
-tile_kernel_fn pick_tile_base(const KParams &p) { return tile::pick<false, false>(p); }
+tile_kernel_fn pick_tile_base(const KParams &p) { return tile::pick<false, tile::kPlain>(p); }
 }  // namespace lmx

@@ -4,5 +4,5 @@
 
 namespace lmx {
 typedef void (*tile_kernel_fn)(const KParams);
-tile_kernel_fn pick_tile_base_mem(const KParams &p) { return tile::pick<false, true>(p); }
+tile_kernel_fn pick_tile_base_mem(const KParams &p) { return tile::pick<false, tile::kMem>(p); }
 }  // namespace lmx

@@ -4,5 +4,5 @@
 
 namespace lmx {
 typedef void (*tile_kernel_fn)(const KParams);
-tile_kernel_fn pick_tile_lemix(const KParams &p) { return tile::pick<true, false>(p); }
+tile_kernel_fn pick_tile_lemix(const KParams &p) { return tile::pick<true, tile::kPlain>(p); }
 }  // namespace lmx

@@ -1,0 +1,9 @@
+// lemix_tile_lemix_cb.cu -- instantiations of the tile event-loop kernel for
+// the LeMix policy with Algorithm 3 continuous batching + decode (see
+// lemix_tile.cuh).
+#include "lemix_tile.cuh"
+
+namespace lmx {
+typedef void (*tile_kernel_fn)(const KParams);
+tile_kernel_fn pick_tile_lemix_cb(const KParams &p) { return tile::pick<true, tile::kCb>(p); }
+}  // namespace lmx

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LMX_LIB") or os.path.join(_HERE, "liblemix.so")
 
 LMX_OK, LMX_EINVAL, LMX_ESTATE, LMX_ENOMEM, LMX_ECUDA, LMX_ENCCL, LMX_EQCAP, LMX_EBUDGET = range(8)
-LMX_LEMIX, LMX_RR, LMX_SEPARATE, LMX_FIXED = range(4)
+LMX_LEMIX, LMX_RR, LMX_SEPARATE, LMX_FIXED, LMX_MIXLUF = range(5)
 LMX_HOST, LMX_DEVICE = 0, 1
 STATUS_NAMES = {0: "LMX_OK", 1: "LMX_EINVAL", 2: "LMX_ESTATE", 3: "LMX_ENOMEM", 4: "LMX_ECUDA",
                 5: "LMX_ENCCL", 6: "LMX_EQCAP", 7: "LMX_EBUDGET"}
@@ -32,13 +32,13 @@ EXPORTS = ("lmx_params_default", "lmx_create", "lmx_destroy", "lmx_last_error", 
 
 class lmx_profile(ctypes.Structure):
     _fields_ = [("n_nodes", ctypes.c_int32), ("n_stages", ctypes.c_int32),
-                ("eta_f", ctypes.c_void_p), ("eta_b", ctypes.c_void_p)]
+                ("eta_f", ctypes.c_void_p), ("eta_b", ctypes.c_void_p), ("eta_d", ctypes.c_void_p)]
 
 
 class lmx_traces(ctypes.Structure):
     _fields_ = [("n_traces", ctypes.c_int64), ("offsets", ctypes.c_void_p), ("n_inf", ctypes.c_void_p),
                 ("arrival", ctypes.c_void_p), ("len_batch_kind", ctypes.c_void_p),
-                ("fixed_node", ctypes.c_void_p)]
+                ("fixed_node", ctypes.c_void_p), ("out_len", ctypes.c_void_p)]
 
 
 class lmx_params(ctypes.Structure):
@@ -50,13 +50,15 @@ class lmx_params(ctypes.Structure):
                 ("mem_dt", ctypes.c_double), ("mem_tmax", ctypes.c_double), ("mem_pen", ctypes.c_double),
                 ("sync_interval", ctypes.c_int32), ("sync_pad", ctypes.c_int32), ("sync_latency", ctypes.c_double),
                 ("sep_dynamic", ctypes.c_int32), ("sep_pad", ctypes.c_int32), ("dyn_rate", ctypes.c_double),
-                ("dyn_window", ctypes.c_double), ("debug_level", ctypes.c_int32), ("debug_pad", ctypes.c_int32)]
+                ("dyn_window", ctypes.c_double), ("debug_level", ctypes.c_int32), ("debug_pad", ctypes.c_int32),
+                ("cb_cmax", ctypes.c_int32), ("eq4_mode", ctypes.c_int32), ("cb_tw", ctypes.c_double),
+                ("luf_delay", ctypes.c_double)]
 
 
 SUMMARY_INT = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version",
-               "status", "n_mem_wait", "n_offload")
+               "status", "n_mem_wait", "n_offload", "n_batches", "n_tbt")
 SUMMARY_F64 = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util",
-               "mean_len_std")
+               "mean_len_std", "sum_tbt", "mean_tbt")
 SUMMARY_DTYPE = np.dtype([(k, np.int64) for k in SUMMARY_INT] + [(k, np.float64) for k in SUMMARY_F64])
 CELL_INT = ("n_traces", "n_failed", "n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals",
             "sum_active_nodes", "sum_version")
@@ -155,13 +157,20 @@ class Params:
     dyn_window: float = 10.0
     # stepwise debug output (lmx_params.debug_level): 1 = (II, R, f) per decision and node
     debug_level: int = 0
+    # Algorithm 3 continuous batching (lmx_params.cb_*); 0 = off
+    cb_cmax: int = 0
+    cb_tw: float = 0.0
+    # Eq. 4 reading (0 = R-14, 1 = R-14b) and Mix-LUF's scheduler latency
+    eq4_mode: int = 0
+    luf_delay: float = 0.0
 
     def c(self) -> lmx_params:
         return lmx_params(self.policy, self.deprioritize, self.slo_mode, self.qcap, self.lambda1, self.lambda2,
                           self.tau, self.slo_mult, self.slo_const, self.sigma_floor, self.lc0, self.alpha,
                           self.mem_enable, 0, self.mem_cap, self.mem_dt, self.mem_tmax, self.mem_pen,
                           self.sync_interval, 0, self.sync_latency, self.sep_dynamic, 0, self.dyn_rate,
-                          self.dyn_window, self.debug_level, 0)
+                          self.dyn_window, self.debug_level, 0, self.cb_cmax, self.eq4_mode, self.cb_tw,
+                          self.luf_delay)
 
 
 class Context:
@@ -192,18 +201,19 @@ class Context:
         except Exception:
             pass
 
-    def lmx_load_profile(self, n_nodes, n_stages, eta_f, eta_b):
+    def lmx_load_profile(self, n_nodes, n_stages, eta_f, eta_b, eta_d=None):
         eta_f = np.ascontiguousarray(eta_f, np.float64)
         eta_b = np.ascontiguousarray(eta_b, np.float64)
-        pr = lmx_profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data)
+        eta_d = None if eta_d is None else np.ascontiguousarray(eta_d, np.float64)
+        pr = lmx_profile(n_nodes, n_stages, eta_f.ctypes.data, eta_b.ctypes.data, _ptr(eta_d))
         return self._check(self.lib.lmx_load_profile(self.h, ctypes.byref(pr)))
 
-    def lmx_load_traces(self, offsets, n_inf, arrival, lbk, fixed_node=None, mem=LMX_HOST):
+    def lmx_load_traces(self, offsets, n_inf, arrival, lbk, fixed_node=None, mem=LMX_HOST, out_len=None):
         offsets = np.ascontiguousarray(offsets, np.int64)
         n_inf = np.ascontiguousarray(n_inf, np.int32)
-        self._keep = [offsets, n_inf, arrival, lbk, fixed_node]
+        self._keep = [offsets, n_inf, arrival, lbk, fixed_node, out_len]
         tr = lmx_traces(len(n_inf), offsets.ctypes.data, n_inf.ctypes.data, _ptr(arrival), _ptr(lbk),
-                        _ptr(fixed_node))
+                        _ptr(fixed_node), _ptr(out_len))
         return self._check(self.lib.lmx_load_traces(self.h, ctypes.byref(tr), mem))
 
     def lmx_set_params(self, params: Params):
@@ -312,17 +322,20 @@ class RunResult:
 
 def run(eta_f, eta_b, n_nodes, n_stages, traces, params: Params | None = None, device: int = 0,
         outputs: bool = True, fixed_node=None, cells=None, n_cells: int = 1, ctx: Context | None = None,
-        cell_params: dict | None = None):
+        cell_params: dict | None = None, eta_d=None):
     """Convenience: create -> load -> run -> sync -> fetch, all through the C ABI.
     `traces` is a workload.Traces (host arrays)."""
     params = params or Params()
     own = ctx is None
     ctx = ctx or Context(device)
     try:
-        ctx.lmx_load_profile(n_nodes, n_stages, eta_f, eta_b)
+        ctx.lmx_load_profile(n_nodes, n_stages, eta_f, eta_b, eta_d)
+        out_len = (np.ascontiguousarray(traces.out_len, np.uint32)
+                   if params.cb_cmax > 0 and traces.out_len is not None else None)
         ctx.lmx_load_traces(traces.offsets, traces.n_inf, np.ascontiguousarray(traces.arrival, np.float64),
                             np.ascontiguousarray(traces.lbk, np.uint32),
-                            None if fixed_node is None else np.ascontiguousarray(fixed_node, np.int32))
+                            None if fixed_node is None else np.ascontiguousarray(fixed_node, np.int32),
+                            out_len=out_len)
         ctx.lmx_set_params(params)
         ctx.lmx_set_cells(cells, n_cells)
         if cell_params is not None:   # {"lambda1": [...], "lambda2": [...], "tau": [...]} per cell

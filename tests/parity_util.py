@@ -7,8 +7,9 @@ import oracle
 import workload
 
 INT_FIELDS = ("n_tasks", "n_inf", "n_train", "n_slo_met", "n_deferrals", "active_nodes", "sum_version", "status",
-              "n_mem_wait", "n_offload")
-F64_FIELDS = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util", "mean_len_std")
+              "n_mem_wait", "n_offload", "n_batches", "n_tbt")
+F64_FIELDS = ("makespan", "throughput", "sum_ttft", "mean_ttft", "slo_attainment", "mean_util", "mean_len_std",
+              "sum_tbt", "mean_tbt")
 REL_TOL = 1e-12   # north_star: fp summaries within 1e-12 relative
 
 
@@ -19,7 +20,8 @@ def oracle_params(lp) -> oracle.OracleParams:
                                slo_const=lp.slo_const, mem_enable=lp.mem_enable, mem_cap=lp.mem_cap,
                                mem_dt=lp.mem_dt, mem_tmax=lp.mem_tmax, mem_pen=lp.mem_pen,
                                sync_interval=lp.sync_interval, sync_latency=lp.sync_latency,
-                               sep_dynamic=lp.sep_dynamic, dyn_rate=lp.dyn_rate, dyn_window=lp.dyn_window)
+                               sep_dynamic=lp.sep_dynamic, dyn_rate=lp.dyn_rate, dyn_window=lp.dyn_window,
+                               cb_cmax=lp.cb_cmax, cb_tw=lp.cb_tw, eq4_mode=lp.eq4_mode, luf_delay=lp.luf_delay)
 
 
 def rel_err(a, b):
@@ -69,16 +71,18 @@ def compare_tasks(traces, g, o_pt, osum, bitwise=True):
             assert bits_equal(gv, ov), f"{k} not bit-identical (rel err {e})"
 
 
-def run_both(N, S, traces, lp, fixed=None, outputs=True, cells=None, n_cells=1):
+def run_both(N, S, traces, lp, fixed=None, outputs=True, cells=None, n_cells=1, eta_d=None):
     from paper_2507_21276_b200 import lemix
     ef, eb = workload.profile(N, S)
-    g = lemix.run(ef, eb, N, S, traces, lp, outputs=outputs, fixed_node=fixed, cells=cells, n_cells=n_cells)
-    osum, opt, ct, _ = oracle.run_batch(ef, eb, N, S, traces, oracle_params(lp), fixed_node=fixed, outputs=outputs)
+    g = lemix.run(ef, eb, N, S, traces, lp, outputs=outputs, fixed_node=fixed, cells=cells, n_cells=n_cells,
+                  eta_d=eta_d)
+    osum, opt, ct, _ = oracle.run_batch(ef, eb, N, S, traces, oracle_params(lp), fixed_node=fixed, outputs=outputs,
+                                        eta_d=eta_d)
     return g, osum, opt, ct
 
 
-def check(N, S, traces, lp, fixed=None, outputs=True, bitwise=True):
-    g, osum, opt, ct = run_both(N, S, traces, lp, fixed, outputs)
+def check(N, S, traces, lp, fixed=None, outputs=True, bitwise=True, eta_d=None):
+    g, osum, opt, ct = run_both(N, S, traces, lp, fixed, outputs, eta_d=eta_d)
     compare_summaries(g.summaries, osum, bitwise=bitwise)
     if outputs:
         compare_tasks(traces, g, opt, osum, bitwise=bitwise)

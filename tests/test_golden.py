@@ -29,6 +29,7 @@ def load(path):
     eb = np.full(N * S, g["eta_b"], np.float64)
     tr = from_lists([[tuple(t) for t in g["tasks"]]])
     g["fixed_np"] = np.asarray(g["fixed"], np.int32) if "fixed" in g else None
+    g["eta_d_np"] = np.full(N * S, g["eta_d"], np.float64) if "eta_d" in g else None
     return g, N, S, ef, eb, tr
 
 
@@ -41,7 +42,7 @@ def test_oracle_matches_golden(path):
     g, N, S, ef, eb, tr = load(path)
     par = oracle.OracleParams(**g["params"])
     o = oracle.run_trace(ef, eb, N, S, tr.arrival, tr.lbk, tr.n_inf[0], par, fixed_node=g["fixed_np"],
-                         want_paths=True, want_cand=True)
+                         want_paths=True, want_cand=True, out_len=tr.out_len, eta_d=g["eta_d_np"])
     assert o["status"] == 0
     ex = g["expect"]
     for task, stages in ex.get("paths", {}).items():
@@ -72,7 +73,7 @@ def test_cuda_path_matches_golden(path):
     lemix = pytest.importorskip("paper_2507_21276_b200.lemix")
     g, N, S, ef, eb, tr = load(path)
     res = lemix.run(ef, eb, N, S, tr, lemix.Params(**g["params"]), device=0, outputs=True,
-                    fixed_node=g["fixed_np"])
+                    fixed_node=g["fixed_np"], eta_d=g["eta_d_np"])
     assert res.status == 0, res.error
     ex = g["expect"]
     node = (res.node_defer & 0xFFFF).astype(int)

@@ -137,3 +137,44 @@ def test_separate_dynamic(rate, window):
     check(4, 2, tr, P(policy=lemix.LMX_SEPARATE, sep_dynamic=1, dyn_rate=rate, dyn_window=window))
     check(8, 2, tr, P(policy=lemix.LMX_SEPARATE, sep_dynamic=1, dyn_rate=rate, dyn_window=window,
                       sync_interval=7, sync_latency=0.5))
+
+
+# ------------------------------------------- NEXT-2 / NEXT-4 / Eq. 4 reading
+CB_POLICIES = [lemix.LMX_LEMIX, lemix.LMX_RR, lemix.LMX_SEPARATE, lemix.LMX_MIXLUF]
+
+
+@pytest.mark.parametrize("N,S", [(4, 2), (2, 4), (8, 8), (64, 2)])
+@pytest.mark.parametrize("policy", CB_POLICIES)
+def test_continuous_batching(N, S, policy):
+    """Algorithm 3 batches + decode steps (DESIGN.md R-cb), bit-exact per
+    request (node, decision, last-token time, start) and per trace (TTFT,
+    SLO, TBT, batches)."""
+    tr = workload.generate(workload.tiny_spec(rate=120.0, n_inf=300), 4, seed_base=17)
+    lp = P(policy=policy, cb_cmax=8, cb_tw=workload.batch_timeout(S), luf_delay=0.002)
+    g, osum, ct = check(N, S, tr, lp, eta_d=workload.decode_profile(N, S))
+    assert osum["n_batches"].sum() < tr.n_inf.sum()     # some requests were batched
+    assert osum["n_tbt"].sum() > 0
+
+
+def test_continuous_batching_sweep_rates():
+    tr = workload.concat([workload.generate(workload.sweep_spec(r), 3, seed_base=60 + int(r)) for r in (20.0, 160.0)])
+    for policy in (lemix.LMX_LEMIX, lemix.LMX_SEPARATE):
+        check(4, 2, tr, P(policy=policy, cb_cmax=16, cb_tw=0.05, sync_interval=5, sync_latency=0.3),
+              eta_d=workload.decode_profile(4, 2))
+
+
+@pytest.mark.parametrize("N,S", [(4, 2), (8, 8)])
+def test_mix_luf(N, S):
+    """Mix-LUF (R-luf) with and without the query latency."""
+    tr = workload.generate(workload.tiny_spec(rate=60.0), 3, seed_base=23)
+    for d in (0.0, 0.076):
+        check(N, S, tr, P(policy=lemix.LMX_MIXLUF, luf_delay=d))
+
+
+@pytest.mark.parametrize("N,S", [(4, 2), (2, 4), (8, 8)])
+def test_eq4_mode1(N, S):
+    """Eq. 4 reading R-14b (the training task's own forward counts)."""
+    tr = workload.concat([workload.generate(workload.mc_spec(True, 400, 400, rate=150.0), 3, seed_base=31),
+                          workload.generate(workload.tiny_spec(rate=80.0), 2, seed_base=32)])
+    g, osum, ct = check(N, S, tr, P(eq4_mode=1))
+    assert osum["n_deferrals"].sum() > 0

@@ -18,16 +18,17 @@ pytestmark = pytest.mark.gpu
 lemix = pytest.importorskip("paper_2507_21276_b200.lemix")
 
 
-def _stepwise(N, S, tr, lp, fixed=None):
+def _stepwise(N, S, tr, lp, fixed=None, eta_d=None):
     ef, eb = workload.profile(N, S)
-    g = lemix.run(ef, eb, N, S, tr, lp, outputs=True, fixed_node=fixed)
+    g = lemix.run(ef, eb, N, S, tr, lp, outputs=True, fixed_node=fixed, eta_d=eta_d)
     assert g.cand is not None
     op = oracle_params(lp)
     n_checked = 0
     for t in range(tr.n_traces):
         a, b = tr.offsets[t], tr.offsets[t + 1]
         o = oracle.run_trace(ef, eb, N, S, tr.arrival[a:b], tr.lbk[a:b], tr.n_inf[t], op,
-                             fixed_node=None if fixed is None else fixed[a:b], want_cand=True)
+                             fixed_node=None if fixed is None else fixed[a:b], want_cand=True,
+                             out_len=tr.out_len[a:b] if lp.cb_cmax > 0 else None, eta_d=eta_d)
         assert o["status"] == g.summaries["status"][t]
         oc, gc = o["cand"], g.cand[a:b]
         nan_o, nan_g = np.isnan(oc), np.isnan(gc)
@@ -116,3 +117,11 @@ def test_response_time_zero_is_invalid():
     assert g.status == lemix.LMX_EINVAL
     assert list(g.summaries["status"]) == list(osum["status"]) == [0, lemix.LMX_EINVAL]
     assert "R <= 0" in g.error
+
+
+def test_stepwise_batching_luf_eq4():
+    tr = workload.generate(workload.tiny_spec(rate=120.0, n_inf=250), 3, seed_base=41)
+    ed = workload.decode_profile(4, 2)
+    for kw in (dict(cb_cmax=8, cb_tw=workload.batch_timeout(2)), dict(eq4_mode=1)):
+        _stepwise(4, 2, tr, lemix.Params(debug_level=1, **kw), eta_d=ed if "cb_cmax" in kw else None)
+    _stepwise(4, 2, tr, lemix.Params(policy=lemix.LMX_MIXLUF, luf_delay=0.01, debug_level=1))

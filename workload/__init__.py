@@ -170,9 +170,10 @@ def concat(parts) -> Traces:
 
 def from_lists(traces) -> Traces:
     """Build a batch from python lists: each trace is a list of
-    (arrival, length, batch, kind) with kind 0 = inference, 1 = training.
-    Tasks are stably partitioned (inference first); inference tasks must be in
-    arrival order, training tasks in release order."""
+    (arrival, length, batch, kind[, out_len]) with kind 0 = inference,
+    1 = training, out_len = decode steps (default 0).  Tasks are stably
+    partitioned (inference first); inference tasks must be in arrival order,
+    training tasks in release order."""
     parts = []
     for tr in traces:
         inf = [t for t in tr if t[3] == 0]
@@ -181,8 +182,9 @@ def from_lists(traces) -> Traces:
         arr = np.array([t[0] for t in rows], np.float64)
         lbk = pack([t[1] for t in rows], [t[2] for t in rows], [t[3] for t in rows]) if rows else \
             np.zeros(0, np.uint32)
+        out = np.array([t[4] if len(t) > 4 else 0 for t in rows], np.uint32)
         parts.append(Traces(np.array([0, len(rows)], np.int64), np.array([len(inf)], np.int32), arr,
-                            lbk, np.zeros(len(rows), np.uint32)))
+                            lbk, out))
     return concat(parts)
 
 
@@ -203,6 +205,22 @@ def profile(n_nodes: int, n_stages: int, model: str = "llama-8b"):
     ef = fwd / 250000.0 * scale
     eb = bwd / 250000.0 * scale
     return (np.full(n_nodes * n_stages, ef, np.float64), np.full(n_nodes * n_stages, eb, np.float64))
+
+
+def decode_profile(n_nodes: int, n_stages: int, model: str = "llama-8b"):
+    """eta_D [N*S] (seconds per context token per item of one decode step on a
+    stage GPU): one decode step of one request at the Table 1
+    reference context (500 tokens) costs 1/20 of that shape's forward, i.e.
+    the model's per-token decode time is ~5% of a 500-token prefill."""
+    fwd, _ = TABLE1[model]
+    return np.full(n_nodes * n_stages, fwd * (2.0 / n_stages) / 20.0 / 500.0, np.float64)
+
+
+def batch_timeout(n_stages: int, model: str = "llama-8b") -> float:
+    """T_w = 0.5 x the inference latency: half the Table 1
+    forward of the whole model at its reference shape."""
+    fwd, _ = TABLE1[model]
+    return 0.5 * fwd * (2.0 / n_stages) * n_stages
 
 
 # --------------------------------------------------------------------------
@@ -296,6 +314,6 @@ def mc_traces_subset(idx, n_total=65536, seed_base=1, n_inf=10000, n_train=10000
     return Traces(offsets, np.full(len(idx), n_inf, np.int32), arrival, lbk, out_len)
 
 
-__all__ = ["mc_traces_subset", "WorkloadSpec", "Traces", "generate", "concat", "from_lists", "pack", "unpack", "profile",
+__all__ = ["mc_traces_subset", "decode_profile", "batch_timeout", "WorkloadSpec", "Traces", "generate", "concat", "from_lists", "pack", "unpack", "profile",
            "tiny_spec", "paper_spec", "sweep_spec", "large_spec", "mc_spec", "mc_traces", "SWEEP_RATES",
            "TABLE1", "replace"]
