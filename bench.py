@@ -335,6 +335,8 @@ def main():
     ap.add_argument("--check-traces", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--config", default="mc", choices=["mc", "sweep", "large", "paper", "mc-cb"],
+                    help="mc (default, the metric's config); the others run tools/bench_configs.py (1 GPU)")
     ap.add_argument("--mem-cap", type=int, default=0,
                     help="> 0: run Algorithm 2 (memory-aware execution) with this many activation tokens per GPU")
     args = ap.parse_args()
@@ -347,6 +349,12 @@ def main():
 
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config != "mc":
+        if rank == 0:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import bench_configs
+            bench_configs.run_config(args.config, args)
         return
 
     import torch

@@ -210,17 +210,18 @@ def profile(n_nodes: int, n_stages: int, model: str = "llama-8b"):
 def decode_profile(n_nodes: int, n_stages: int, model: str = "llama-8b"):
     """eta_D [N*S] (seconds per context token per item of one decode step on a
     stage GPU): one decode step of one request at the Table 1
-    reference context (500 tokens) costs 1/20 of that shape's forward, i.e.
-    the model's per-token decode time is ~5% of a 500-token prefill."""
+    reference context (500 tokens) costs 1/200 of that shape's forward (0.55 ms
+    per Llama-8B stage at S = 2), so a 200-token output over a ~100-token
+    context keeps a stage busy ~0.1 s."""
     fwd, _ = TABLE1[model]
-    return np.full(n_nodes * n_stages, fwd * (2.0 / n_stages) / 20.0 / 500.0, np.float64)
+    return np.full(n_nodes * n_stages, fwd * (2.0 / n_stages) / 200.0 / 500.0, np.float64)
 
 
-def batch_timeout(n_stages: int, model: str = "llama-8b") -> float:
-    """T_w = 0.5 x the inference latency: half the Table 1
-    forward of the whole model at its reference shape."""
-    fwd, _ = TABLE1[model]
-    return 0.5 * fwd * (2.0 / n_stages) * n_stages
+def batch_timeout(n_stages: int, model: str = "llama-8b", length: int = 64) -> float:
+    """T_w = 0.5 x the inference latency of the median request
+    (a `length`-token prompt, C = 1) through all stages: 0.5 * S * eta_F * l^2."""
+    ef, _ = profile(1, n_stages, model)
+    return 0.5 * float(ef[0]) * n_stages * length * length
 
 
 # --------------------------------------------------------------------------
