@@ -57,7 +57,8 @@ typedef enum {
     LMX_ECUDA = 4,    /* CUDA runtime error */
     LMX_ENCCL = 5,    /* NCCL unavailable or failed */
     LMX_EQCAP = 6,    /* per trace: a node's training queue Q_train^n exceeded params.qcap */
-    LMX_EBUDGET = 7   /* per trace: decision budget exhausted (cannot happen for valid input) */
+    LMX_EBUDGET = 7,  /* per trace: decision budget exhausted (cannot happen for valid input) */
+    LMX_ETIMEOUT = 8  /* per trace: streamed host inputs did not land within 60 s (a copy never completed) */
 } lmx_status;
 
 /* LMX_MIXLUF: the Mix-LUF comparison system (DESIGN.md

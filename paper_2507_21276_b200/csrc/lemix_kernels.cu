@@ -21,6 +21,8 @@
 
 #include <climits>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "lemix_tile.cuh"
 
@@ -95,11 +97,26 @@ kernel_fn pick_tile_lemix_mem(const KParams &p);
 kernel_fn pick_tile_base_mem(const KParams &p);
 kernel_fn pick_tile_lemix_cb(const KParams &p);
 kernel_fn pick_tile_base_cb(const KParams &p);
+kernel_fn pick_fast(const KParams &p);
+bool fast_applies(const KParams &p);
+int fast_smem_bytes(const KParams &p);
 
 namespace {
 
+// LMX_KERNEL=generic (developer override): the tile kernel for every run,
+// also where the one-node-per-lane LeMix kernel applies
+bool use_fast(const KParams &p)
+{
+    static const bool generic = [] {
+        const char *e = getenv("LMX_KERNEL");
+        return e != nullptr && strcmp(e, "generic") == 0;
+    }();
+    return !generic && fast_applies(p);
+}
+
 kernel_fn pick(const KParams &p)
 {
+    if (use_fast(p)) return pick_fast(p);
     if (p.mem_enable) return p.policy == LMX_LEMIX ? pick_tile_lemix_mem(p) : pick_tile_base_mem(p);
     if (p.cb_cmax > 0) return p.policy == LMX_LEMIX ? pick_tile_lemix_cb(p) : pick_tile_base_cb(p);
     return p.policy == LMX_LEMIX ? pick_tile_lemix(p) : pick_tile_base(p);
@@ -113,6 +130,7 @@ int npl_bucket(int npl) { return tile::npl_bucket(npl); }
 
 int event_loop_smem_bytes(const KParams &p)
 {
+    if (use_fast(p)) return fast_smem_bytes(p);
     const int W = tile::window_entries(p.S);
     const int npl = npl_bucket(p.npl);
     return (int)tile::profile_bytes(p.N * p.S, p.cb_cmax > 0) + (W > 0 ? kBlock * npl * W * ring_words(p.S, p.mem_enable != 0) * 16 : 0) +

@@ -198,14 +198,14 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 t = (long long)tt;
                 const long long o = p.offsets[t];
                 const int len = (int)(p.offsets[t + 1] - o);
-                dev::wait_inputs(p.ready, p.chunk_tasks, o, o + len);
+                const bool landed = dev::wait_inputs(p.ready, p.chunk_tasks, o, o + len);
                 nI = p.n_inf[t];
                 nT = len - nI;
                 tarr = p.arrival + o;
                 tlbk = p.lbk + o;
                 i = j = step = iters = rr = sep_i = sep_t = cur_defer = 0;
                 rate_lo = rate_hi = 0;
-                status = LMX_OK;
+                status = landed ? LMX_OK : LMX_ETIMEOUT;
                 dev::sts_l(c_tw(0), t);
                 dev::sts_l(c_tw(1), o);
                 dev::sts_l(c_tw(3), kErrNone);
@@ -218,10 +218,12 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 sum_ttft = 0.0;
                 t_last = -kInf;
                 a_last_inf = -kInf;
-                if (nI > 0) { a_inf = __ldg(tarr); v_inf = __ldg(tlbk); }
-                if (nI > 1) { a_inf2 = __ldg(tarr + 1); v_inf2 = __ldg(tlbk + 1); }
-                if (nT > 0) { a_tr = __ldg(tarr + nI); v_tr = __ldg(tlbk + nI); }
-                if (nT > 1) { a_tr2 = __ldg(tarr + nI + 1); v_tr2 = __ldg(tlbk + nI + 1); }
+                if (landed) {
+                    if (nI > 0) { a_inf = __ldg(tarr); v_inf = __ldg(tlbk); }
+                    if (nI > 1) { a_inf2 = __ldg(tarr + 1); v_inf2 = __ldg(tlbk + 1); }
+                    if (nT > 0) { a_tr = __ldg(tarr + nI); v_tr = __ldg(tlbk + nI); }
+                    if (nT > 1) { a_tr2 = __ldg(tarr + nI + 1); v_tr2 = __ldg(tlbk + nI + 1); }
+                }
                 r = (nT > 0) ? a_tr : kInf;
                 double t_first = kInf;
                 if (nI > 0) t_first = dev::dmin(t_first, a_inf);

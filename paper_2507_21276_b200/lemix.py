@@ -17,11 +17,12 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # LMX_LIB: developer override (A/B of alternative builds of the same sources)
 LIB_PATH = os.environ.get("LMX_LIB") or os.path.join(_HERE, "liblemix.so")
 
-LMX_OK, LMX_EINVAL, LMX_ESTATE, LMX_ENOMEM, LMX_ECUDA, LMX_ENCCL, LMX_EQCAP, LMX_EBUDGET = range(8)
+LMX_OK, LMX_EINVAL, LMX_ESTATE, LMX_ENOMEM, LMX_ECUDA, LMX_ENCCL, LMX_EQCAP, LMX_EBUDGET, LMX_ETIMEOUT = range(9)
 LMX_LEMIX, LMX_RR, LMX_SEPARATE, LMX_FIXED, LMX_MIXLUF = range(5)
 LMX_HOST, LMX_DEVICE = 0, 1
 STATUS_NAMES = {0: "LMX_OK", 1: "LMX_EINVAL", 2: "LMX_ESTATE", 3: "LMX_ENOMEM", 4: "LMX_ECUDA",
-                5: "LMX_ENCCL", 6: "LMX_EQCAP", 7: "LMX_EBUDGET"}
+                5: "LMX_ENCCL", 6: "LMX_EQCAP", 7: "LMX_EBUDGET",
+                8: "LMX_ETIMEOUT"}
 
 EXPORTS = ("lmx_params_default", "lmx_create", "lmx_destroy", "lmx_last_error", "lmx_load_profile",
            "lmx_load_traces", "lmx_set_params", "lmx_set_cells", "lmx_set_cell_params", "lmx_set_outputs", "lmx_run", "lmx_sync",
