@@ -619,8 +619,8 @@ lmx_status lmx_run(lmx_ctx *c)
                                       cudaGetErrorString((cudaError_t)occ_err));
     int n_sm = 0;
     cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, c->device);
-    const int block = lmx::event_loop_block_threads();
-    const int tiles_per_block = block / k.T;
+    const int block = lmx::event_loop_block_threads(k);
+    const int tiles_per_block = lmx::event_loop_traces_per_block(k);
     int64_t grid = (int64_t)n_sm * per_sm;
     const int64_t need = (T + tiles_per_block - 1) / tiles_per_block;
     grid = std::max<int64_t>(1, std::min(grid, need));

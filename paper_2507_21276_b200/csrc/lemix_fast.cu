@@ -1,5 +1,6 @@
 // lemix_fast.cu -- instantiations of the one-node-per-lane LeMix kernel
-// (see lemix_fast.cuh): pipeline depth S in {1, 2, 4} x tile width T.
+// (see lemix_fast.cuh): pipeline depth S in {1, 2, 4} x tile width T (one-warp
+// tiles), and the wide kernel, S in {2, 4, 8} x 2 or 4 warps per trace.
 #include "lemix_fast.cuh"
 
 namespace lmx {
@@ -17,8 +18,19 @@ static tile_kernel_fn pick_fast_t(int T)
     }
 }
 
+template <int TW>
+static tile_kernel_fn pick_wide(int S)
+{
+    switch (S) {
+    case 2: return fast::fast_loop_kernel<2, 32, TW>;
+    case 4: return fast::fast_loop_kernel<4, 32, TW>;
+    default: return fast::fast_loop_kernel<8, 32, TW>;
+    }
+}
+
 tile_kernel_fn pick_fast(const KParams &p)
 {
+    if (p.N > 32) return fast::tile_warps(p) == 2 ? pick_wide<2>(p.S) : pick_wide<4>(p.S);
     switch (p.S) {
     case 1: return pick_fast_t<1>(p.T);
     case 2: return pick_fast_t<2>(p.T);
@@ -27,5 +39,6 @@ tile_kernel_fn pick_fast(const KParams &p)
 }
 
 bool fast_applies(const KParams &p) { return fast::applies(p); }
-int fast_smem_bytes(const KParams &p) { return fast::smem_bytes(p.N, p.S); }
+int fast_smem_bytes(const KParams &p) { return fast::smem_bytes(p.N, p.S, fast::tile_warps(p)); }
+int fast_block_threads(const KParams &p) { return fast::block_threads(fast::tile_warps(p)); }
 }  // namespace lmx

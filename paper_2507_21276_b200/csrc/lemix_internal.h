@@ -94,7 +94,8 @@ struct CellParams {
 int max_stages_bucket(int S);                         // template bucket for S
 int npl_bucket(int npl);                              // template bucket for nodes/lane
 int event_loop_smem_bytes(const KParams &p);
-int event_loop_block_threads();
+int event_loop_block_threads(const KParams &p);
+int event_loop_traces_per_block(const KParams &p);   // traces in flight per CTA
 // blocks per SM the event loop can keep resident with this geometry
 int event_loop_occupancy(const KParams &p, int *err);
 int launch_event_loop(const KParams &p, int grid, void *stream);

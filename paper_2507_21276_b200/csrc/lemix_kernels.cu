@@ -100,6 +100,7 @@ kernel_fn pick_tile_base_cb(const KParams &p);
 kernel_fn pick_fast(const KParams &p);
 bool fast_applies(const KParams &p);
 int fast_smem_bytes(const KParams &p);
+int fast_block_threads(const KParams &p);
 
 namespace {
 
@@ -137,7 +138,13 @@ int event_loop_smem_bytes(const KParams &p)
            kBlock * (npl * tile::cold_words(p.S, npl > 1) + (p.cell_par ? tile::kTraceWords : 4)) * 8;
 }
 
-int event_loop_block_threads() { return kBlock; }
+int event_loop_block_threads(const KParams &p) { return use_fast(p) ? fast_block_threads(p) : kBlock; }
+
+int event_loop_traces_per_block(const KParams &p)
+{
+    // the wide kernel (several warps per trace) places one trace per CTA
+    return use_fast(p) && p.N > 32 ? 1 : event_loop_block_threads(p) / p.T;
+}
 
 int event_loop_occupancy(const KParams &p, int *err)
 {
@@ -145,7 +152,7 @@ int event_loop_occupancy(const KParams &p, int *err)
     const int smem = event_loop_smem_bytes(p);
     cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int blocks = 0;
-    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, kBlock, smem);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, f, event_loop_block_threads(p), smem);
     *err = (int)e;
     return blocks;
 }
@@ -154,7 +161,7 @@ int launch_event_loop(const KParams &p, int grid, void *stream)
 {
     kernel_fn f = pick(p);
     const int smem = event_loop_smem_bytes(p);
-    f<<<grid, kBlock, smem, (cudaStream_t)stream>>>(p);
+    f<<<grid, event_loop_block_threads(p), smem, (cudaStream_t)stream>>>(p);
     return (int)cudaGetLastError();
 }
 
