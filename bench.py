@@ -44,9 +44,9 @@ UNIT = "decisions/s"
 # and exp_neg count their fixed fp64 instruction expansions on sm_100a
 # (cuobjdump -sass of the kernel, profiles/r02_fp64_expansions.txt): div.rn.f64
 # = MUFU.RCP64H + 7 DFMA + 1 DMUL = 9, sqrt.rn.f64 = MUFU.RSQ64H + 8 DFMA/DMUL
-# = 9, exp_neg = 36 (clamp, 2 scale mul/sub pairs, rint, 26 Estrin mul/add, 2^k
+# = 9, exp_neg = 38 (16 DADD + 20 DMUL + DSETP + FRND: clamp, scale, rint, Estrin, 2^k
 # scale, cutoff select).
-DIV, SQRT, EXP = 9, 9, 36
+DIV, SQRT, EXP = 9, 9, 38
 OP_WEIGHTS = {
     "decisions": 1 + 1 + 1 + 1,  # event select compare; t_last MAX; release MAX; ready/defer compare
     "stage_iters": 6,            # dF mul, start MAX, end add, II: sub, sub, add
@@ -70,6 +70,21 @@ def ops_per_decision(counters: dict) -> float:
     total = sum(OP_WEIGHTS[k] * counters[k] for k in OP_WEIGHTS)
     total += COMMIT_OPS * counters["decisions"]
     return total / max(1, counters["decisions"])
+
+
+def fp64_peak(n_sm, sm_mhz):
+    """The fp64 pipe's measured throughput (tools/ubench/fp64_peak.cu on this
+    pool's B200: independent DADD chains over every SM, profiles/r02_fp64_peak.json),
+    else the nominal 64 DP lanes/clk/SM x SMs x clock."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_fp64_peak.json")) as f:
+            pk = json.load(f)
+        return float(pk["dadd_tops"]), (f"measured DADD throughput {pk['dadd_tops']:.2f} T/s "
+                                         f"(tools/ubench/fp64_peak.cu, profiles/r02_fp64_peak.json; "
+                                         f"nominal {pk['nominal_64_lanes_tops']:.2f})")
+    except (OSError, KeyError, ValueError):
+        t = 64 * n_sm * sm_mhz * 1e6 / 1e12
+        return t, f"nominal 64 DP lanes/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz = {t:.2f} T/s"
 
 
 def measured_peaks():
@@ -506,7 +521,7 @@ def main():
         peaks, peak_src = measured_peaks()
         sm_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         n_sm = torch.cuda.get_device_properties(local_rank).multi_processor_count
-        peak_tflops = 64 * n_sm * sm_mhz * 1e6 / 1e12     # fp64 lanes/clk/SM x SMs x clock
+        peak_tflops, peak_note = fp64_peak(n_sm, sm_mhz)
         k_s = statistics.mean(kernel_ms) / 1e3
         achieved = opd * M / k_s / 1e12
         traffic = None
@@ -519,11 +534,11 @@ def main():
             pass
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                     "frac": achieved / peak_tflops, "traffic": traffic,
-                    "kernel": f"lmx::tile::event_loop_kernel<2, true, 1, true, 4, {str(bool(args.mem_cap)).lower()}>",
+                    "kernel": ("lmx::tile::event_loop_kernel<2, true, 1, true, 4, 1>" if args.mem_cap
+                               else "lmx::fast::fast_loop_kernel<2, 4, 1>"),
                     "note": (f"fp64 pipe: {opd:.1f} algorithmic fp64 ops/decision (oracle counters x DESIGN.md "
                              f"weights; div/sqrt/exp = their SASS expansions {DIV}/{SQRT}/{EXP}) x {M} decisions / "
-                             f"{k_s * 1e3:.1f} ms mean kernel time; peak = 64 "
-                             f"DP lanes/clk/SM x {n_sm} SMs x {sm_mhz:.0f} MHz ({peak_src} clock); "
+                             f"{k_s * 1e3:.1f} ms mean kernel time; peak = {peak_note}; "
                              f"HBM bound {M * 12 / k_s / 1e9:.0f} GB/s of {peaks.get('hbm_gbs')}"),
                     "max_queue_depth_sample": counters["max_qlen"]}
 

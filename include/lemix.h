@@ -264,11 +264,32 @@ lmx_status lmx_set_cell_params(lmx_ctx *ctx, int32_t n_cells, const double *lamb
 /* Optional: keep per-task outputs (default on).  Off = summary-only runs. */
 lmx_status lmx_set_outputs(lmx_ctx *ctx, int per_task);
 
-/* Run every trace (one persistent kernel) and reduce per-cell summaries. */
+/* Run every trace and reduce the per-cell summaries; asynchronous on the
+ * context stream (LMX_ESTATE before profile, traces and params are loaded).
+ * One persistent kernel runs the discrete-event loop of each trace: at every
+ * decision point the next task (inference by arrival; training released at
+ * the previous training task's S1 forward end) is deprioritised
+ * by Eq. 4 or placed -- LeMix: Algorithm 1 ComputeIdleness
+ * on every node, Eq. 1-3, the highest
+ * f, lowest node on ties; RR / Separate / Fixed / Mix-LUF: PAPER.md:795-797
+ * -- and committed (backward planning).  Algorithm 2
+ * with params.mem_enable, Algorithm 3
+ * with params.cb_cmax.  Returns LMX_OK when enqueued; per-trace failures
+ * (LMX_EINVAL on bad task data, LMX_EQCAP, LMX_EBUDGET, LMX_ETIMEOUT) are
+ * reported by lmx_sync and the summaries' status.  Outputs are a pure
+ * function of (profile, traces, params): no launch-geometry or GPU-count
+ * dependence (the cross-rank fp64 cell sums aside, see lmx_allreduce_cells). */
 lmx_status lmx_run(lmx_ctx *ctx);
+/* Wait for the last lmx_run; returns its first non-OK per-trace status (the
+ * lowest failing trace, named with its task and field by lmx_last_error) --
+ * the other traces' results stay valid -- or LMX_ECUDA on a device error.
+ * Releases the borrow of HOST / DEVICE task arrays. */
 lmx_status lmx_sync(lmx_ctx *ctx);
 
-/* Per-task outputs, indexed like the task arrays.  node_defer = node index
+/* Per-task outputs (the assignment and completion times of SPEC.md:23's task
+ * records; TTFT = completion - arrival for inference), indexed
+ * like the task arrays, valid after lmx_sync (LMX_ESTATE before, or when the
+ * run was summary-only).  node_defer = node index
  * (bits 0-15) | Eq. 4 deferral count saturated at 0xFFFF (bits 16-31);
  * decision_idx = the decision (0-based, per trace) that placed the task;
  * completion = inference end_f^S, training end_b^1; start_f1 = start_f^1.
@@ -287,14 +308,22 @@ lmx_status lmx_get_times(lmx_ctx *ctx, double *completion, double *start_f1, lmx
  * destination lives.  LMX_ESTATE unless the last run had debug_level 1. */
 lmx_status lmx_get_candidates(lmx_ctx *ctx, double *cand, lmx_mem mem);
 
-/* Per-trace summaries [n_traces] (host memory). */
+/* Per-trace summaries [n_traces] (host memory; the metrics of PAPER.md:786-790:
+ * throughput, SLO attainment with TTFT <= tau_R, mean TTFT, utilisation,
+ * active nodes PAPER.md:569-573, the loss proxies of SPEC.md:439), valid after
+ * lmx_sync.  SURVEY.md 8(b)'s `total` argument is lmx_get_cells (one cell =
+ * all traces unless lmx_set_cells grouped them). */
 lmx_status lmx_get_summaries(lmx_ctx *ctx, lmx_summary *per_trace);
-/* Per-cell aggregates [n_cells] (host memory). */
+/* Per-cell aggregates [n_cells] (host memory), valid after lmx_sync: integer
+ * sums exact, fp64 sums over the cell's traces in trace order. */
 lmx_status lmx_get_cells(lmx_ctx *ctx, lmx_cell_summary *cells);
 
-/* Multi-GPU: one grouped ncclAllReduce(sum) of the cell aggregates over
- * `nccl_comm` (an ncclComm_t) on the context stream.  NCCL is resolved at run
- * time (dlopen "libnccl.so.2"); LMX_ENCCL if unavailable. */
+/* Multi-GPU (8(b) calls it lmx_allreduce_summaries): one
+ * grouped ncclAllReduce(sum) of the cell aggregates over `nccl_comm` (an
+ * ncclComm_t) on the context stream, after lmx_sync.  Integer fields are exact
+ * for any rank count; the fp64 sums depend on the NCCL reduction order (within
+ * 1e-12 relative of a single-GPU run).  NCCL is resolved at run time (dlopen
+ * "libnccl.so.2"); LMX_ENCCL if unavailable. */
 lmx_status lmx_allreduce_cells(lmx_ctx *ctx, void *nccl_comm);
 /* Helpers to build a communicator without a framework: rank 0 calls
  * lmx_nccl_unique_id, ships the 128 bytes to every rank, each calls

@@ -168,7 +168,7 @@ def run_config(name, args):
     peaks, _ = bench.measured_peaks()
     mhz = float(peaks.get("sm_max_mhz", 1965.0))
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
-    peak = 64 * n_sm * mhz * 1e6 / 1e12
+    peak, peak_note = bench.fp64_peak(n_sm, mhz)
     k_s = [statistics.mean(k[r] for k in kern) / 1e3 for r in range(len(runs))]
     achieved = sum(o * tr.n_tasks for o in opd) / sum(k_s) / 1e12
     line = {"metric": bench.METRIC, "value": decisions / step_s, "unit": bench.UNIT, "n_gpus": 1,
@@ -180,7 +180,7 @@ def run_config(name, args):
             "traces_per_s": tr.n_traces * len(runs) / step_s,
             "kernel_ms": {r[0]: round(k * 1e3, 3) for r, k in zip(runs, k_s)},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak,
+                         "frac": achieved / peak, "peak_note": peak_note,
                          "ops_per_decision": {r[0]: round(o, 1) for r, o in zip(runs, opd)}},
             "parity": parity, "clocks": sampler.report()}
     print(json.dumps(line), flush=True)
