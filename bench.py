@@ -535,7 +535,7 @@ def main():
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak_tflops, "unit": "TFLOP/s",
                     "frac": achieved / peak_tflops, "traffic": traffic,
                     "kernel": ("lmx::tile::event_loop_kernel<2, true, 1, true, 4, 1>" if args.mem_cap
-                               else "lmx::fast::fast_loop_kernel<2, 4, 1>"),
+                               else "lmx::fast::fast_loop_kernel<2, 4, 1, true>"),
                     "note": (f"fp64 pipe: {opd:.1f} algorithmic fp64 ops/decision (oracle counters x DESIGN.md "
                              f"weights; div/sqrt/exp = their SASS expansions {DIV}/{SQRT}/{EXP}) x {M} decisions / "
                              f"{k_s * 1e3:.1f} ms mean kernel time; peak = {peak_note}; "

@@ -611,6 +611,8 @@ lmx_status lmx_run(lmx_ctx *c)
     k.fixed = c->has_fixed ? (const int32_t *)c->fixed.p : nullptr;
     k.eta = (const double *)c->eta.p;
 
+    k.want_outputs = c->per_task;
+    k.want_cand = P.debug_level == 1;
     // geometry: persistent grid = resident CTAs, capped by the number of traces
     int occ_err = 0;
     const int per_sm = lmx::event_loop_occupancy(k, &occ_err);

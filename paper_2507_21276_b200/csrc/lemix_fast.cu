@@ -6,15 +6,15 @@
 namespace lmx {
 typedef void (*tile_kernel_fn)(const KParams);
 
-template <int S>
+template <int S, bool LEAN>
 static tile_kernel_fn pick_fast_t(int T)
 {
     switch (T) {
-    case 2: return fast::fast_loop_kernel<S, 2>;
-    case 4: return fast::fast_loop_kernel<S, 4>;
-    case 8: return fast::fast_loop_kernel<S, 8>;
-    case 16: return fast::fast_loop_kernel<S, 16>;
-    default: return fast::fast_loop_kernel<S, 32>;
+    case 2: return fast::fast_loop_kernel<S, 2, 1, LEAN>;
+    case 4: return fast::fast_loop_kernel<S, 4, 1, LEAN>;
+    case 8: return fast::fast_loop_kernel<S, 8, 1, LEAN>;
+    case 16: return fast::fast_loop_kernel<S, 16, 1, LEAN>;
+    default: return fast::fast_loop_kernel<S, 32, 1, LEAN>;
     }
 }
 
@@ -31,10 +31,11 @@ static tile_kernel_fn pick_wide(int S)
 tile_kernel_fn pick_fast(const KParams &p)
 {
     if (p.N > 32) return fast::tile_warps(p) == 2 ? pick_wide<2>(p.S) : pick_wide<4>(p.S);
+    const bool lean = fast::lean(p);
     switch (p.S) {
-    case 1: return pick_fast_t<1>(p.T);
-    case 2: return pick_fast_t<2>(p.T);
-    default: return pick_fast_t<4>(p.T);
+    case 1: return lean ? pick_fast_t<1, true>(p.T) : pick_fast_t<1, false>(p.T);
+    case 2: return lean ? pick_fast_t<2, true>(p.T) : pick_fast_t<2, false>(p.T);
+    default: return lean ? pick_fast_t<4, true>(p.T) : pick_fast_t<4, false>(p.T);
     }
 }
 

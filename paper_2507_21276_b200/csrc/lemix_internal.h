@@ -72,6 +72,9 @@ struct KParams {
 
     double2 *ring_be;          // [tile_slots][Npad][K][ring_words(S)]: (start_b, end_b) per stage, dB pairs
     int32_t npad;              // npl * T
+    // the run writes per-task outputs / debug candidates (set before the
+    // kernel is picked, so geometry queries and the launch pick the same one)
+    int32_t want_outputs, want_cand;
 };
 
 // field codes for trace_err (reported by lmx_last_error)

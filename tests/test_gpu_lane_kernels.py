@@ -53,6 +53,14 @@ def test_lane_kernels_bitexact(N, S):
         check(N, S, tr, lemix.Params(qcap=4096, eq4_mode=1, tau=-0.01))
 
 
+@pytest.mark.parametrize("N,S", [(2, 1), (4, 2), (5, 4), (32, 2)])
+def test_lane_kernels_summary_only(N, S):
+    """Summary-only runs take the LEAN instantiation (no per-task outputs, no
+    debug output, R-14, per-task tau_R compiled out): summaries bitwise."""
+    for heavy in (False, True):
+        check(N, S, traces(90 + N, heavy), lemix.Params(qcap=4096), outputs=False)
+
+
 @pytest.mark.parametrize("N,S", [(4, 2), (32, 4), (64, 8), (128, 2)])
 def test_lane_kernels_stepwise(N, S):
     """Every candidate's (II, R, f) at every decision, bitwise."""
