@@ -18,20 +18,23 @@ static tile_kernel_fn pick_fast_t(int T)
     }
 }
 
-template <int TW>
+template <int TW, bool LEAN>
 static tile_kernel_fn pick_wide(int S)
 {
     switch (S) {
-    case 2: return fast::fast_loop_kernel<2, 32, TW>;
-    case 4: return fast::fast_loop_kernel<4, 32, TW>;
-    default: return fast::fast_loop_kernel<8, 32, TW>;
+    case 2: return fast::fast_loop_kernel<2, 32, TW, LEAN>;
+    case 4: return fast::fast_loop_kernel<4, 32, TW, LEAN>;
+    default: return fast::fast_loop_kernel<8, 32, TW, LEAN>;
     }
 }
 
 tile_kernel_fn pick_fast(const KParams &p)
 {
-    if (p.N > 32) return fast::tile_warps(p) == 2 ? pick_wide<2>(p.S) : pick_wide<4>(p.S);
     const bool lean = fast::lean(p);
+    if (p.N > 32) {
+        if (fast::tile_warps(p) == 2) return lean ? pick_wide<2, true>(p.S) : pick_wide<2, false>(p.S);
+        return lean ? pick_wide<4, true>(p.S) : pick_wide<4, false>(p.S);
+    }
     switch (p.S) {
     case 1: return lean ? pick_fast_t<1, true>(p.T) : pick_fast_t<1, false>(p.T);
     case 2: return lean ? pick_fast_t<2, true>(p.T) : pick_fast_t<2, false>(p.T);

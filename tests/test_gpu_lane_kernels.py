@@ -53,7 +53,7 @@ def test_lane_kernels_bitexact(N, S):
         check(N, S, tr, lemix.Params(qcap=4096, eq4_mode=1, tau=-0.01))
 
 
-@pytest.mark.parametrize("N,S", [(2, 1), (4, 2), (5, 4), (32, 2)])
+@pytest.mark.parametrize("N,S", [(2, 1), (4, 2), (5, 4), (32, 2), (64, 8), (100, 2)])
 def test_lane_kernels_summary_only(N, S):
     """Summary-only runs take the LEAN instantiation (no per-task outputs, no
     debug output, R-14, per-task tau_R compiled out): summaries bitwise."""
