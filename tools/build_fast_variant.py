@@ -23,7 +23,7 @@ if r.returncode:
 lines = r.stdout.splitlines() + r.stderr.splitlines()
 for k, ln in enumerate(lines):   # the bench instantiation's resources
     if "ILi2ELi4E" in ln and "Function properties" in ln:
-        print(tag, lines[k + 1].strip(), "|", lines[k + 2].strip())
+        print(tag, "LEAN" if "Lb1E" in ln else "full", lines[k + 1].strip(), "|", lines[k + 2].strip())
 objs = [o for o in glob.glob(os.path.join(bdir, "*.o")) if not o.endswith("lemix_fast.o")] + [obj]
 subprocess.run(["/usr/local/cuda/bin/nvcc", *ARCH, "-shared", *objs, "-o", os.path.join(PKG, f"liblemix_{tag}.so"),
                 "-lcudart", "-ldl"], check=True)
