@@ -534,6 +534,41 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                 // serially by the winning lane in the commit
                 double mu_n[NPL], kk_n[NPL], cc_n[NPL];
                 long long sl_n[NPL], sl2_n[NPL];
+                bool ok_st = true;   // LMX_FASTDIV: every division / sqrt took its fast path
+                auto spec_stats = [&](long long c, long long a1, long long a2, int jj) {
+                    sl_n[jj] = a1;
+                    sl2_n[jj] = a2;
+                    const long long var = c * a2 - a1 * a1;
+                    if (LMX_FASTDIV) {
+                        bool ok1, ok2, ok3;
+                        const double inv_c = dev::rcp_fastpath((double)c, ok1);
+                        mu_n[jj] = (double)a1 * inv_c;
+                        // (sqrt(+0) = +0: the argument is made nonzero, the fast path would not take 0)
+                        double sq = dev::sqrt_fastpath((double)(var == 0 ? 1 : var), ok2);
+                        sq = (var == 0) ? 0.0 : sq;
+                        const double sigma = dev::dmax(sq * inv_c, p.sigma_floor);
+                        const double inv_s = dev::rcp_fastpath(sigma, ok3);
+                        kk_n[jj] = (0.5 * inv_s) * inv_s;
+                        cc_n[jj] = inv_s * dev::kInvSqrt2Pi;
+                        ok_st = ok1 && ok2 && ok3;
+                    } else {
+                        const double inv_c = 1.0 / (double)c;
+                        mu_n[jj] = (double)a1 * inv_c;
+                        const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
+                        const double inv_s = 1.0 / sigma;
+                        kk_n[jj] = (0.5 * inv_s) * inv_s;
+                        cc_n[jj] = inv_s * dev::kInvSqrt2Pi;
+                    }
+                };
+                auto spec_stats_ieee = [&](long long c, long long a1, long long a2, int jj) {
+                    const long long var = c * a2 - a1 * a1;
+                    const double inv_c = 1.0 / (double)c;
+                    mu_n[jj] = (double)a1 * inv_c;
+                    const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
+                    const double inv_s = 1.0 / sigma;
+                    kk_n[jj] = (0.5 * inv_s) * inv_s;
+                    cc_n[jj] = inv_s * dev::kInvSqrt2Pi;
+                };
 #pragma unroll
                 for (int jj = 0; jj < NPL; ++jj) {
                     const int n = tl + jj * T;
@@ -587,28 +622,43 @@ __global__ void __launch_bounds__(kBlock, (SMAX >= 4 || NPL > 1) ? 2 : LMX_TILE_
                             const double lam2 = cpar ? dev::lds_d(c_tw(5)) : p.lambda2;
                             const double tau = cpar ? dev::lds_d(c_tw(6)) : p.tau;
                             const double IP = -dev::dmax(IIS - (a - a_last), tau);        // Eq. 1
-                            const double f = (IP + lam2 * LC) / (lam1 * R);               // Eq. 3
+                            const double num = IP + lam2 * LC, den = lam1 * R;
+                            double f;                                                     // Eq. 3
+                            bool ok_f = true;
+                            if (LMX_FASTDIV) {
+                                // (see lemix_device.cuh; a zero numerator has the signed-zero
+                                // quotient for a finite nonzero denominator)
+                                const bool z = num == 0.0;
+                                f = dev::div_fastpath(z ? 1.0 : num, den, ok_f);
+                                f = z ? __longlong_as_double((__double_as_longlong(num) ^ __double_as_longlong(den)) &
+                                                             (long long)0x8000000000000000ull)
+                                      : f;
+                            } else {
+                                f = num / den;
+                            }
+                            // speculative statistics: count + members, sums + their l, l^2
+                            const long long c = cnt[jj] + (CB ? mb : 1);
+                            const long long a1 = dev::lds_l(c_sl(jj)) + (CB ? sum_l : l);
+                            const long long a2 = dev::lds_l(c_sl2(jj)) + (CB ? sum_l2 : (long long)l * l);
+                            spec_stats(c, a1, a2, jj);
+                            if (LMX_FASTDIV && !(ok_f && ok_st)) {
+                                f = num / den;
+                                spec_stats_ieee(c, a1, a2, jj);
+                            }
                             r_bad |= !(R > 0.0);
                             if (n_best == INT_MAX || f > f_best) { f_best = f; n_best = n; }
                             if (p.cand)   // debug_level 1: this candidate's (II, R, f) (uniform branch)
                                 dev::put_cand(p.cand, (dev::lds_l(c_tw(1)) + step) * N + n, II, R, f);
-                        } else if (p.cand) {
-                            dev::put_cand(p.cand, (dev::lds_l(c_tw(1)) + step) * N + n, II,
-                                          dev::last_of(en_s[jj], S) - a, __longlong_as_double(-1ll));
-                        }
-                        {   // speculative statistics: count + members, sums + their l, l^2
+                        } else {
+                            if (p.cand)
+                                dev::put_cand(p.cand, (dev::lds_l(c_tw(1)) + step) * N + n, II,
+                                              dev::last_of(en_s[jj], S) - a, __longlong_as_double(-1ll));
+                            // speculative statistics: count + members, sums + their l, l^2
                             const long long c = cnt[jj] + (CB ? mb : 1);
                             const long long a1 = dev::lds_l(c_sl(jj)) + (CB ? sum_l : l);
                             const long long a2 = dev::lds_l(c_sl2(jj)) + (CB ? sum_l2 : (long long)l * l);
-                            sl_n[jj] = a1;
-                            sl2_n[jj] = a2;
-                            const double inv_c = 1.0 / (double)c;
-                            mu_n[jj] = (double)a1 * inv_c;
-                            const long long var = c * a2 - a1 * a1;
-                            const double sigma = dev::dmax(sqrt((double)var) * inv_c, p.sigma_floor);
-                            const double inv_s = 1.0 / sigma;
-                            kk_n[jj] = (0.5 * inv_s) * inv_s;
-                            cc_n[jj] = inv_s * dev::kInvSqrt2Pi;
+                            spec_stats(c, a1, a2, jj);
+                            if (LMX_FASTDIV && !ok_st) spec_stats_ieee(c, a1, a2, jj);
                         }
                     }
                 }

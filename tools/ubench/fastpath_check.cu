@@ -40,11 +40,11 @@ __global__ void check(uint64_t seed, long long n, unsigned long long *bad, unsig
         const int m1 = (int)(r3 % 5), m2 = (int)((r3 >> 8) % 5);
         const double x = pick(r1, m1), y = pick(r2, m2);
         bool ok;
-        double v = lmx::fast::rcp_fastpath(x, ok);
+        double v = lmx::dev::rcp_fastpath(x, ok);
         if (ok) { t++; b += __double_as_longlong(v) != __double_as_longlong(1.0 / x); }
-        v = lmx::fast::div_fastpath(x, y, ok);
+        v = lmx::dev::div_fastpath(x, y, ok);
         if (ok) { t++; b += __double_as_longlong(v) != __double_as_longlong(x / y); }
-        v = lmx::fast::sqrt_fastpath(fabs(x), ok);
+        v = lmx::dev::sqrt_fastpath(fabs(x), ok);
         if (ok) { t++; b += __double_as_longlong(v) != __double_as_longlong(sqrt(fabs(x))); }
     }
     atomicAdd(bad, b);
