@@ -178,3 +178,20 @@ def test_eq4_mode1(N, S):
                           workload.generate(workload.tiny_spec(rate=80.0), 2, seed_base=32)])
     g, osum, ct = check(N, S, tr, P(eq4_mode=1))
     assert osum["n_deferrals"].sum() > 0
+
+
+# ------------------------------------------- division / sqrt fast-path fallbacks
+# The kernels form Eq. 3's quotient and Eq. 2's 1/cnt, sqrt and 1/sigma through
+# branch-free replicas of ptxas's fast paths and recompute with the IEEE
+# operations when a fast-path predicate fails (shortcut 5).
+# A tiny tau makes IP = -tau on idle nodes, so Eq. 3's numerator is below the
+# fast path's range in most decisions: the fallback branch runs, on the
+# one-node-per-lane kernel (4 x 2), the wide kernel (40 x 8) and the generic
+# tile kernel (Algorithm 2 on), with per-task outputs and summaries.
+@pytest.mark.parametrize("kw", [dict(tau=2.0 ** -1000), dict(tau=2.0 ** -1000, lambda1=2.0 ** -60, lambda2=2.0 ** 40)])
+@pytest.mark.parametrize("N,S,extra", [(4, 2, {}), (40, 8, {}),
+                                       (4, 2, dict(mem_enable=1, mem_cap=800, mem_dt=0.0055, mem_tmax=0.55,
+                                                   mem_pen=8.8e-5))])
+def test_division_fallbacks(kw, N, S, extra):
+    tr = workload.generate(workload.sweep_spec(120.0), 6, seed_base=41)
+    check(N, S, tr, P(**kw, **extra))
