@@ -195,3 +195,28 @@ def test_eq4_mode1(N, S):
 def test_division_fallbacks(kw, N, S, extra):
     tr = workload.generate(workload.sweep_spec(120.0), 6, seed_base=41)
     check(N, S, tr, P(**kw, **extra))
+
+
+# Summary-only runs take the LEAN instantiations: the same traces stop with the
+# same status as the oracle and the same error (task index and field) as the
+# per-task-output instantiations, on one-warp tiles and the wide kernel, for
+# each kind of defect.
+@pytest.mark.parametrize("N,S", [(4, 2), (40, 8)])
+@pytest.mark.parametrize("defect", ["len0", "kind", "order", "negative"])
+def test_invalid_input_summary_only(N, S, defect):
+    tr = workload.generate(workload.tiny_spec(), 4, seed_base=3)
+    o1, o2 = tr.offsets[1], tr.offsets[2]
+    if defect == "len0":
+        tr.lbk[o1 + 7] = workload.pack(0, 1, 0)
+    elif defect == "kind":
+        tr.lbk[o2 + 3] = workload.pack(64, 1, 1)                # an inference slot marked training
+    elif defect == "order":
+        tr.arrival[o1 + 9] = 0.5 * tr.arrival[o1 + 8]            # inference arrivals out of order
+    else:
+        tr.arrival[o2 + 2] = -1.0
+    g, osum, _ = check(N, S, tr, P(), outputs=False)
+    bad = np.nonzero(osum["status"] != 0)[0]
+    assert len(bad) == 1
+    assert np.array_equal(g.summaries["status"], osum["status"])
+    g2, _, _ = check(N, S, tr, P(), outputs=True)                # the outputs path (validation first)
+    assert g.error == g2.error and g.status == g2.status
