@@ -13,6 +13,13 @@ ef8, eb8 = workload.profile(8, 8)
 g = lemix.run(ef8, eb8, 8, 8, tr, lemix.Params(), outputs=True); print("8x8 status", g.status)
 ef64, eb64 = workload.profile(64, 2)
 g = lemix.run(ef64, eb64, 64, 2, tr, lemix.Params(), outputs=True); print("64x2 status", g.status)
+# round 2: summary-only (LEAN) one-warp tiles and wide kernels (two-barrier decision),
+# and the IEEE fallback of the division / sqrt fast paths (tiny tau)
+for (N, S) in ((4, 2), (40, 8), (64, 2), (100, 4)):
+    efn, ebn = workload.profile(N, S)
+    for kw in (dict(), dict(tau=2.0 ** -1000), dict(qcap=3)):
+        g = lemix.run(efn, ebn, N, S, tr, lemix.Params(**kw), outputs=False)
+        print(N, S, "summary-only", kw, "status", g.status)
 PY
 for tool in memcheck racecheck synccheck initcheck; do
   echo "== $tool"
